@@ -1,0 +1,85 @@
+// Kernel-level C-ABI hooks: run one layer kernel on host buffers. Used by the
+// per-kernel parity tests (tests/test_kernels_gpu.py) and by the latency
+// profiler; the serving path goes through bs_step instead.
+#include <cstring>
+#include <vector>
+
+#include "../kernels/conv_tc.cuh"
+#include "bs_exec.h"
+#include "errors.hpp"
+
+using bs200::ConvParams;
+
+extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_host,
+                              const float* w_host, const float* bias_host, const float* res_host,
+                              float* out_host, int reps, float* ms_per_launch) {
+  using namespace bs200;
+  if (!d || nimg <= 0 || !in_host || !w_host || !out_host) return bs_fail(BS_EINVAL, "bs_kernel_conv: null argument");
+  const int K = d->KH * d->KW * d->Cin;
+  const int Kpad = (K + 31) / 32 * 32;
+  const size_t in_img = static_cast<size_t>(d->H) * d->W * d->in_ldc;
+  const size_t out_img = static_cast<size_t>(d->Ho) * d->Wo * d->out_ldc;
+  const size_t res_img = res_host ? static_cast<size_t>(d->Ho) * d->Wo * d->res_ldc : 0;
+  float *din = nullptr, *dw = nullptr, *db = nullptr, *dout = nullptr, *dres = nullptr;
+  float** ptrs = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = BS_OK;
+#define CK(x)                                           \
+  do {                                                  \
+    cudaError_t _e = (x);                               \
+    if (_e != cudaSuccess) {                            \
+      rc = bs_fail_cuda(_e, #x);                        \
+      goto done;                                        \
+    }                                                   \
+  } while (0)
+  {
+    CK(cudaMalloc(&din, in_img * nimg * sizeof(float)));
+    CK(cudaMalloc(&dw, static_cast<size_t>(d->N) * Kpad * sizeof(float)));
+    CK(cudaMalloc(&dout, out_img * nimg * sizeof(float)));
+    if (bias_host) CK(cudaMalloc(&db, d->N * sizeof(float)));
+    if (res_host) CK(cudaMalloc(&dres, res_img * nimg * sizeof(float)));
+    CK(cudaMalloc(&ptrs, 3 * nimg * sizeof(float*)));
+    CK(cudaMemcpy(din, in_host, in_img * nimg * sizeof(float), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw, w_host, static_cast<size_t>(d->N) * Kpad * sizeof(float), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dout, out_host, out_img * nimg * sizeof(float), cudaMemcpyHostToDevice));
+    if (bias_host) CK(cudaMemcpy(db, bias_host, d->N * sizeof(float), cudaMemcpyHostToDevice));
+    if (res_host) CK(cudaMemcpy(dres, res_host, res_img * nimg * sizeof(float), cudaMemcpyHostToDevice));
+    std::vector<float*> hp(3 * nimg);
+    for (int i = 0; i < nimg; ++i) {
+      hp[i] = din + in_img * i;
+      hp[nimg + i] = dout + out_img * i;
+      hp[2 * nimg + i] = dres ? dres + res_img * i : nullptr;
+    }
+    CK(cudaMemcpy(ptrs, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice));
+    ConvParams p{};
+    p.nimg = nimg;
+    p.H = d->H; p.W = d->W; p.Cin = d->Cin; p.Ho = d->Ho; p.Wo = d->Wo;
+    p.KH = d->KH; p.KW = d->KW; p.stride = d->stride; p.pad = d->pad;
+    p.K = K; p.Kpad = Kpad; p.N = d->N;
+    p.in_ptrs = ptrs; p.in_ldc = d->in_ldc; p.in_coff = d->in_coff;
+    p.wgt = dw; p.bias = db;
+    p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_coff = d->out_coff;
+    p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_coff = d->res_coff;
+    p.relu = d->relu; p.round_out = d->round_out;
+    CK(launch_conv_tc(p, 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));
+    if (reps > 0 && ms_per_launch) {
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0));
+      for (int r = 0; r < reps; ++r) CK(launch_conv_tc(p, 0));
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      *ms_per_launch = ms / reps;
+    }
+  }
+#undef CK
+done:
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaFree(din); cudaFree(dw); cudaFree(db); cudaFree(dout); cudaFree(dres); cudaFree(ptrs);
+  return rc;
+}

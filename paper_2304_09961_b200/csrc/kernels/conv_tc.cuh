@@ -1,0 +1,259 @@
+// Implicit-GEMM convolution / fully-connected layer on the sm_100a tensor
+// cores (tcgen05.mma kind::tf32, accumulator in TMEM).
+//
+//   D[m, n] = sum_k A[m, k] * W[n, k]      m = (image, ho, wo), n = out channel,
+//                                          k = (kh, kw, ci) with ci fastest
+//
+// A is never materialised: producer warps gather 16-byte channel chunks of
+// the NHWC input straight into 128B-swizzled shared memory with cp.async
+// (zero-fill implements spatial padding and M/K tails). Every image of the
+// merged batch has its own base pointer, so requests stay in their own
+// activation-arena slots: the batch is "gathered" by the loader and
+// "scattered" by the epilogue, with no copy kernels (SURVEY.md §2.2,
+// gather/scatter row).
+//
+// Warp roles (256 threads):
+//   warps 0-3  producers: A (activations) + B (weights) -> smem ring
+//   warp  4    TMEM allocation; lane 0 issues tcgen05.mma
+//   warps 4-7  epilogue: tcgen05.ld -> bias / residual / ReLU / TF32 round
+//              -> per-image output slot (channel-slice writes give concat
+//              for free).
+#pragma once
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace bs200 {
+
+struct ConvParams {
+  int nimg;                     // images in the merged batch
+  int H, W, Cin;                // input spatial size; Cin = padded channel count (% 4 == 0)
+  int Ho, Wo;                   // output spatial size
+  int KH, KW, stride, pad;
+  int K;                        // KH * KW * Cin
+  int Kpad;                     // K rounded up to 32 (row stride of wgt)
+  int N;                        // output channels
+  const float* const* in_ptrs;  // [nimg] image base pointers
+  int in_ldc, in_coff;          // floats per pixel, first channel
+  const float* wgt;             // [N][Kpad], TF32-rounded, zero padded
+  const float* bias;            // [N] or nullptr
+  float* const* out_ptrs;       // [nimg]
+  int out_ldc, out_coff;
+  const float* const* res_ptrs; // [nimg] or nullptr (residual add before ReLU)
+  int res_ldc, res_coff;
+  int relu;                     // 0 none, 1 ReLU, 2 ReLU6
+  int round_out;                // round outputs to TF32 (they feed another GEMM)
+};
+
+namespace conv_tc {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int kThreads = 256;
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int kABytes = kBM * 128;
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = STAGES * kStageBytes;
+  static constexpr int kTotal = kBarOffset + 256 + 1024;  // barriers + alignment slack
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const ConvParams p) {
+  using S = Smem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* accum_bar = empty_bar + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int M = p.nimg * p.Ho * p.Wo;
+  const int m_base = blockIdx.x * kBM;
+  const int n_base = blockIdx.y * BN;
+  const int KT = p.Kpad / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 128);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    ptx::mbar_init(accum_bar, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 4) ptx::tmem_alloc<BN>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ producers
+    const int t = threadIdx.x;
+    const int c = t & 7;       // 16-byte chunk inside the 128-byte K row
+    const int r0 = t >> 3;     // rows r0 + 16 i
+    const int HoWo = p.Ho * p.Wo;
+    const float* row_base[8];
+    int row_h[8], row_w[8];
+    bool row_ok[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m_base + r0 + 16 * i;
+      row_ok[i] = m < M;
+      const int mm = row_ok[i] ? m : 0;
+      const int n = mm / HoWo;
+      const int rem = mm - n * HoWo;
+      const int ho = rem / p.Wo;
+      const int wo = rem - ho * p.Wo;
+      row_h[i] = ho * p.stride - p.pad;
+      row_w[i] = wo * p.stride - p.pad;
+      row_base[i] = p.in_ptrs[n] + p.in_coff;
+    }
+    const uint32_t smem_base = ptx::smem_u32(smem);
+    constexpr int kBRowsPerThread = BN / 16;
+
+    auto issue = [&](int kt, int s) {
+      const uint32_t a_tile = smem_base + s * S::kStageBytes;
+      const uint32_t b_tile = a_tile + S::kABytes;
+      const int k0 = kt * kBK + c * 4;
+      const bool k_ok = k0 < p.K;
+      int ci = 0, kh = 0, kw = 0;
+      if (k_ok) {
+        const int q = k0 / p.Cin;
+        ci = k0 - q * p.Cin;
+        kh = q / p.KW;
+        kw = q - kh * p.KW;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = r0 + 16 * i;
+        const int h = row_h[i] + kh;
+        const int w = row_w[i] + kw;
+        const bool ok = k_ok && row_ok[i] && h >= 0 && h < p.H && w >= 0 && w < p.W;
+        const float* src = ok ? row_base[i] + (h * p.W + w) * p.in_ldc + ci : p.wgt;
+        const uint32_t dst = a_tile + row * 128 + ((c ^ (row & 7)) << 4);
+        ptx::cp_async16(dst, src, ok ? 16u : 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < kBRowsPerThread; ++j) {
+        const int row = r0 + 16 * j;
+        const int n = n_base + row;
+        const bool ok = n < p.N;
+        const float* src = ok ? p.wgt + static_cast<size_t>(n) * p.Kpad + kt * kBK + c * 4 : p.wgt;
+        const uint32_t dst = b_tile + row * 128 + ((c ^ (row & 7)) << 4);
+        ptx::cp_async16(dst, src, ok ? 16u : 0u);
+      }
+      ptx::cp_async_commit();
+    };
+
+    // Keep up to LAG stages of cp.async in flight per thread; a stage is
+    // published (proxy fence + arrive) once this thread's copies landed.
+    constexpr int LAG = STAGES - 1;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      if (kt >= STAGES) ptx::mbar_wait(&empty_bar[s], ((kt / STAGES) - 1) & 1);
+      issue(kt, s);
+      if (kt >= LAG) {
+        ptx::cp_async_wait<LAG>();
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&full_bar[(kt - LAG) % STAGES]);
+      }
+    }
+    ptx::cp_async_wait<0>();
+    ptx::fence_proxy_async_smem();
+    for (int kt = (KT > LAG ? KT - LAG : 0); kt < KT; ++kt) ptx::mbar_arrive(&full_bar[kt % STAGES]);
+  } else {
+    if (warp == 4) {
+      // ---------------------------------------------------------- MMA issue
+      constexpr uint32_t idesc = ptx::make_idesc(2, kBM, BN);
+      const uint32_t smem_base = ptx::smem_u32(smem);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        ptx::mbar_wait(&full_bar[s], (kt / STAGES) & 1);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_tile = smem_base + s * S::kStageBytes;
+          const uint32_t b_tile = a_tile + S::kABytes;
+          const uint64_t a_desc = ptx::sw128_kmajor_desc(a_tile);
+          const uint64_t b_desc = ptx::sw128_kmajor_desc(b_tile);
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            // +32 bytes per K=8 step inside the swizzled row (>>4 -> +2).
+            ptx::mma_tf32(tmem_base, a_desc + 2 * k, b_desc + 2 * k, idesc, (kt | k) != 0);
+          }
+          ptx::mma_commit(&empty_bar[s]);
+          if (kt == KT - 1) ptx::mma_commit(accum_bar);
+        }
+        __syncwarp();
+      }
+    }
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;
+    const int m = m_base + row;
+    const bool m_ok = m < M;
+    int n_img = 0, pix = 0;
+    if (m_ok) {
+      const int HoWo = p.Ho * p.Wo;
+      n_img = m / HoWo;
+      pix = m - n_img * HoWo;
+    }
+    ptx::mbar_wait(accum_bar, 0);
+    ptx::tc_fence_after();
+    float* out_row = m_ok ? p.out_ptrs[n_img] + static_cast<size_t>(pix) * p.out_ldc + p.out_coff : nullptr;
+    const float* res_row = (m_ok && p.res_ptrs)
+                               ? p.res_ptrs[n_img] + static_cast<size_t>(pix) * p.res_ldc + p.res_coff
+                               : nullptr;
+#pragma unroll 1
+    for (int j = 0; j < BN / 32; ++j) {
+      uint32_t v[32];
+      ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + j * 32, v);
+      ptx::tmem_ld_wait();
+      const int n0 = n_base + j * 32;
+      if (!m_ok || n0 >= p.N) continue;
+      const int ncols = min(32, p.N - n0);
+      float o[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        float x = __uint_as_float(v[q]);
+        if (q < ncols) {
+          if (p.bias) x += __ldg(p.bias + n0 + q);
+          if (res_row) x += res_row[n0 + q];
+          if (p.relu == 1) x = fmaxf(x, 0.f);
+          else if (p.relu == 2) x = fminf(fmaxf(x, 0.f), 6.f);
+          if (p.round_out) x = ptx::round_tf32(x);
+        }
+        o[q] = x;
+      }
+      float* dst = out_row + n0;
+      if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 32; q += 4)
+          *reinterpret_cast<float4*>(dst + q) = make_float4(o[q], o[q + 1], o[q + 2], o[q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < ncols) dst[q] = o[q];
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<BN>(tmem_base);
+  }
+}
+
+}  // namespace conv_tc
+
+// Host-side launcher; picks the N tile by output width.
+cudaError_t launch_conv_tc(const ConvParams& p, cudaStream_t stream);
+
+}  // namespace bs200
