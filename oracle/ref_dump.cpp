@@ -192,6 +192,32 @@ json do_call(const json& c, const ProfileSet& ps) {
       for (int k = 1; k <= n; ++k)
         for (int b = 1; b <= bound + 1; ++b) v.push_back(bits(ps.lookup(dnn, k, b)));
       out["result"] = v;
+    } else if (fn == "rng") {
+      SplitMix64 g = c.contains("tag") ? SplitMix64::stream(c.at("seed").get<std::uint64_t>(), c.at("tag").get<std::uint64_t>())
+                                       : SplitMix64(c.at("seed").get<std::uint64_t>());
+      json v = json::array();
+      for (int i = 0; i < c.value("count", 4); ++i) {
+        const std::uint64_t a = g.next_u64();
+        char buf[24];
+        std::snprintf(buf, sizeof buf, "%016" PRIx64, a);
+        v.push_back(std::string(buf));
+        v.push_back(bits(g.next_double()));
+        v.push_back(bits(g.exponential(3.5)));
+        v.push_back(bits(g.pareto(1.25, 0.2)));
+        v.push_back(g.uniform_int(-3, 17));
+      }
+      out["result"] = v;
+    } else if (fn == "arrivals") {
+      WorkloadSpec spec;
+      spec.process = parse_process(c.value("process", std::string("poisson")));
+      spec.rate = c.value("rate", 100.0);
+      spec.count = c.value("count", 50);
+      spec.seed = c.value("seed", std::uint64_t{1});
+      if (c.contains("dnn_mix"))
+        for (const auto& m : c.at("dnn_mix")) spec.dnn_mix.emplace_back(m.at(0).get<std::string>(), m.at(1).get<double>());
+      json v = json::array();
+      for (const auto& a : generate_arrivals(spec)) v.push_back(json::array({bits(a.time), a.dnn, a.size_bits}));
+      out["result"] = v;
     } else {
       throw std::invalid_argument("unknown fn " + fn);
     }

@@ -72,3 +72,24 @@ def fptr(a) -> "C._Pointer":
         return None
     assert a.dtype.name == "float32" and a.flags["C_CONTIGUOUS"]
     return a.ctypes.data_as(FP)
+
+
+def host_call(job: dict | str) -> str:
+    """Run one JSON job through libbs_host.so (bs_host_call); returns JSONL."""
+    import json as _json
+    lib = host_lib()
+    if not getattr(lib, "_bs_declared", False):
+        lib.bs_host_call.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.bs_host_call.restype = C.c_int
+        lib.bs_host_free.argtypes = [C.c_void_p]
+        lib.bs_host_last_error.restype = C.c_char_p
+        lib._bs_declared = True
+    text = job if isinstance(job, str) else _json.dumps(job)
+    out = C.c_void_p()
+    rc = lib.bs_host_call(text.encode(), C.byref(out))
+    if rc != 0:
+        raise BsError(f"bs_host_call status {rc}: {lib.bs_host_last_error().decode()}")
+    try:
+        return C.string_at(out).decode()
+    finally:
+        lib.bs_host_free(out)

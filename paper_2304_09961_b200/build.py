@@ -21,6 +21,11 @@ CSRC = PKG / "csrc"
 LIB = PKG / "lib"
 OBJ = ROOT / "build" / "obj"
 INCLUDE = ROOT / "include"
+# nlohmann/json (header-only parser; the copy shipped in this image's
+# cudnn_frontend tree, the same one the reference oracle is built with).
+JSON_INC = Path(os.environ.get(
+    "BS_JSON_INC",
+    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -71,7 +76,8 @@ def _compile(src: Path, digest: str) -> Path:
     obj = OBJ / (str(rel).replace("/", "__") + ".o")
     obj.parent.mkdir(parents=True, exist_ok=True)
     if _needs(obj, src, digest):
-        incs = [f"-I{INCLUDE}", f"-I{CSRC}", f"-I{CSRC / 'host'}", f"-I{CSRC / 'exec'}"]
+        incs = [f"-I{INCLUDE}", f"-I{CSRC}", f"-I{CSRC / 'host'}", f"-I{CSRC / 'exec'}",
+                f"-I{JSON_INC}"]
         if src.suffix == ".cu":
             cmd = [NVCC, *NVCC_FLAGS, *incs, "-c", str(src), "-o", str(obj)]
         else:
