@@ -1,17 +1,31 @@
 /* C ABI of the B200 batched-layer executor (libbs_exec.so).
  *
  * The reference (batchsim, arXiv 2304.09961) has no executor: a batched step
- * is a cost-table lookup scheduled as a completion event
- * (proj/include/batchsim/simulator.hpp:533-539 start_step,
- *  :702-721 step_duration, :475-516 on_step_complete).
- * These entry points are what replaces that lookup: the host event loop calls
- * bs_admit where arrive_at_server runs (simulator.hpp:447-465), bs_step where
- * start_step fires, bs_retire where finish runs (simulator.hpp:740-751) and
- * bs_drop where drop_expired / tardy drops resolve a request
- * (simulator.hpp:548-559, :611-628).
+ * is a cost-table lookup scheduled as a completion event. Each entry point
+ * below replaces one point of the reference's serving loop
+ * (proj/include/batchsim/simulator.hpp):
+ *
+ *   bs_admit      arrive_at_server        simulator.hpp:447-465 (request enters the
+ *                                         queue at entry_layer; entry_layer > 1 is the
+ *                                         collaborative path, :325-371 / :393-419)
+ *   bs_plan       compute_plan            simulator.hpp:541-570 (a new plan discards
+ *                                         in-progress rides: riders rewind)
+ *   bs_step       start_step              simulator.hpp:533-539 (instead of
+ *                                         scheduling now + sum_k h_k(b), run layers
+ *                                         [from, to] with the batch rule of
+ *                                         step_duration, :702-721)
+ *   bs_step_done  on_step_complete        simulator.hpp:497-511 (rider deposits)
+ *   bs_retire     finish                  simulator.hpp:740-751
+ *   bs_drop       drop_expired / tardy    deadline.hpp:21-35, simulator.hpp:611-628
+ *   bs_profile_layer / bs_profile_table   the h_k(b) grids of the cost model
+ *                                         (cost_model.hpp:22-82, profile_io.hpp:3-18)
+ *   bs_replay     run_sim                 simulator.hpp:787-792, every step executed
+ *   bs_serve      (new) the same loop on the wall clock
  *
  * Plain C types only; every function returns a status code (BS_OK == 0) and
  * bs_last_error() holds the text of the most recent failure on this thread.
+ * Calls on one handle must be serialised by the caller (one host thread per
+ * GPU); GPU work is asynchronous on the handle's stream.
  */
 #ifndef BS_EXEC_H_
 #define BS_EXEC_H_
@@ -32,7 +46,65 @@ enum {
   BS_ESTATE = -5    /* unknown request / order -> std::logic_error      */
 };
 
+typedef struct bs_handle bs_handle;
+
+/* A segment member: request id and the layer it currently sits at. */
+typedef struct bs_member {
+  int64_t id;
+  int layer;
+} bs_member;
+
+/* A foreign request carried through a shared stage (schedule.hpp:24-30). */
+typedef struct bs_rider {
+  int64_t id;
+  int dnn;
+  int join_layer;
+  int leave_layer;
+  int deposit_layer;
+} bs_rider;
+
 const char* bs_last_error(void);
+void bs_free(char* p);
+
+/* ---------------------------------------------------------------- handle */
+
+/* suite: "small_cnn", "googlenet", "resnet50", "mobilenet_v2",
+ * "resnet50_pair", "hetero3", "collab". max_requests = arena slots. */
+int bs_create(int device, const char* suite, int max_batch, int max_requests, bs_handle** out);
+int bs_destroy(bs_handle* h);
+/* JSON: DNNs, layers, ops, tensor plan, weight offsets (for checkers). */
+int bs_suite_json(bs_handle* h, char** out_json);
+int bs_read_weights(bs_handle* h, float* dst, size_t n);
+/* The deterministic synthetic image for (seed, index). */
+int bs_make_image(uint64_t seed, uint64_t index, int H, int W, int C, int real_c, float* out);
+
+/* ------------------------------------------------------------- requests */
+
+int bs_admit(bs_handle* h, int64_t id, int dnn, int entry_layer, const float* image_host);
+int bs_plan(bs_handle* h, int plan_no);
+int bs_step(bs_handle* h, int plan_no, int segment, int dnn, int layer_from, int layer_to,
+            const bs_member* members, int n_members, const bs_rider* riders, int n_riders);
+int bs_step_done(bs_handle* h, const int64_t* deposited, int n);
+/* Copies the request's class probabilities (or logits) out and frees its slot. */
+int bs_retire(bs_handle* h, int64_t id, float* out, int n, int logits);
+int bs_drop(bs_handle* h, int64_t id);
+int bs_read_blob(bs_handle* h, int64_t id, float* dst, size_t n);
+int bs_sync(bs_handle* h);
+
+/* ----------------------------------------------------------- measurement */
+
+int bs_profile_layer(bs_handle* h, int dnn, int layer, int batch, int reps, int flush_l2, double* ms);
+/* opts: {"batches": [...], "reps": r, "flush_l2": bool} -> reference-schema profile JSON */
+int bs_profile_table(bs_handle* h, const char* opts_json, char** out_json);
+
+/* ------------------------------------------------------------- serving */
+
+/* Virtual-time run_sim (bit-exact reference schedules) with every step
+ * executed; job JSON as bs_host_call's "sim" job plus "image_seed",
+ * "image_pool", "dump_ids". Returns JSONL (outcomes, results, summary). */
+int bs_replay(bs_handle* h, const char* job_json, char** out_jsonl);
+/* Live wall-clock serving of the same job description on the GPU. */
+int bs_serve(bs_handle* h, const char* job_json, char** out_json);
 
 /* ---------------------------------------------------------------- kernels */
 

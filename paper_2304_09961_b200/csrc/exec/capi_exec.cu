@@ -1,0 +1,335 @@
+// C-ABI of libbs_exec.so (declared in include/bs_exec.h).
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+
+#include "bs_exec.h"
+#include "bsb/jobs.hpp"
+#include "errors.hpp"
+#include "executor.hpp"
+#include "image.hpp"
+#include "live.hpp"
+
+using json = nlohmann::json;
+using namespace bs200;
+
+struct bs_handle {
+  std::unique_ptr<Executor> ex;
+};
+
+namespace {
+
+char* dup_str(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::invalid_argument& e) {
+    return bs_fail(BS_EINVAL, e.what());
+  } catch (const std::logic_error& e) {
+    return bs_fail(BS_ESTATE, e.what());
+  } catch (const std::bad_alloc& e) {
+    return bs_fail(BS_ENOMEM, e.what());
+  } catch (const std::exception& e) {
+    const std::string w = e.what();
+    return bs_fail(w.find("full") != std::string::npos ? BS_ENOMEM : BS_ECUDA, w);
+  }
+}
+
+json suite_json(const Suite& s, std::size_t blob_floats) {
+  json nets = json::array();
+  for (const NetDef& n : s.nets) {
+    json tensors = json::array();
+    for (const TensorDef& t : n.tensors)
+      tensors.push_back({{"name", t.name}, {"H", t.H}, {"W", t.W}, {"C", t.C}, {"off", t.off}});
+    json ops = json::array();
+    for (const OpDef& o : n.ops) {
+      const char* kind = o.kind == OpKind::conv      ? "conv"
+                         : o.kind == OpKind::maxpool ? "maxpool"
+                         : o.kind == OpKind::avgpool ? "avgpool"
+                         : o.kind == OpKind::dwconv  ? "dwconv"
+                                                     : "softmax";
+      auto ref = [](const TRef& r) { return json::array({r.t, r.coff, r.C}); };
+      ops.push_back({{"kind", kind}, {"name", o.name}, {"in", ref(o.in)}, {"out", ref(o.out)}, {"res", ref(o.res)},
+                     {"k", o.KH}, {"stride", o.stride}, {"pad", o.pad}, {"relu", o.relu},
+                     {"round_out", o.round_out}, {"ceil", o.ceil_mode}, {"Kpad", o.Kpad}, {"w_off", o.w_off},
+                     {"b_off", o.b_off}, {"Ho", o.Ho}, {"Wo", o.Wo}, {"flops", o.flops_per_image},
+                     {"weight_floats", o.weight_floats}});
+    }
+    json layers = json::array();
+    for (const LayerDef& l : n.layers)
+      layers.push_back({{"name", l.name}, {"ops", l.ops}, {"component", l.component}, {"offset", l.offset}});
+    nets.push_back({{"name", n.name}, {"components", n.components}, {"tensors", tensors}, {"ops", ops},
+                    {"layers", layers}, {"input", n.input_t}, {"logits", n.logits_t}, {"probs", n.probs_t},
+                    {"in_H", n.in_H}, {"in_W", n.in_W}, {"in_C", n.in_C}, {"classes", n.num_classes},
+                    {"blob_floats", n.blob_floats}});
+  }
+  json comps = json::array();
+  for (const ComponentDef& c : s.components) comps.push_back({{"id", c.id}, {"num_layers", c.num_layers}});
+  return {{"suite", s.name}, {"components", comps}, {"nets", nets}, {"weights", s.weights.size()},
+          {"slot_floats", blob_floats}, {"max_batch", s.max_batch}};
+}
+
+// Virtual-time serving (the reference's event loop, bit-exact schedules)
+// with every step executed on the GPU.
+struct ReplayHook : batchsim::StepHook {
+  Executor* ex;
+  std::vector<int> dnn_map;  // profile dnn -> suite net
+  std::uint64_t image_seed = 1;
+  bool pool = true;
+  float* results = nullptr;  // pinned [count][classes]
+  int classes = 0;
+  std::vector<float> host_img;
+  int max_batch_seen = 0;
+  long steps = 0;
+
+  void admit(batchsim::RequestId id, int dnn, int entry_layer, batchsim::Ms) override {
+    const int net = dnn_map[static_cast<std::size_t>(dnn)];
+    const NetDef& nd = ex->suite().nets[static_cast<std::size_t>(net)];
+    if (pool && ex->pool_size(net) > 0) {
+      ex->admit(id, net, entry_layer, ex->pool_image(net, static_cast<int>((id - 1) % ex->pool_size(net))), true);
+    } else {
+      host_img.resize(static_cast<std::size_t>(nd.in_H) * nd.in_W * nd.in_C);
+      synth_image(image_seed, static_cast<std::uint64_t>(id - 1), nd.in_H, nd.in_W, nd.in_C, 3, host_img.data());
+      ex->admit(id, net, entry_layer, host_img.data(), false);
+      ex->sync();  // host buffer is reused
+    }
+  }
+  void plan(int plan_no, batchsim::Ms) override { ex->new_plan(plan_no); }
+  void step(const batchsim::StepView& v) override {
+    ex->step(v.plan, v.segment, dnn_map[static_cast<std::size_t>(v.dnn)], v.from, v.to, v.members, v.riders);
+    max_batch_seen = std::max(max_batch_seen, static_cast<int>(v.members.size() + v.riders.size()));
+    ++steps;
+  }
+  void step_done(const batchsim::StepView&, const std::vector<batchsim::RequestId>& dep) override {
+    ex->step_done(dep);
+  }
+  void finish(batchsim::RequestId id, batchsim::Ms) override {
+    if (ex->has(id)) ex->retire_async(id, results + static_cast<std::size_t>(id - 1) * classes, classes);
+  }
+  void drop(batchsim::RequestId id, batchsim::Ms) override { ex->drop(id); }
+};
+
+std::vector<int> map_dnns(const batchsim::ProfileSet& ps, const Suite& s) {
+  std::vector<int> m;
+  for (const auto& d : ps.dnns) {
+    int idx = -1;
+    for (std::size_t i = 0; i < s.nets.size(); ++i)
+      if (s.nets[i].name == d.name()) idx = static_cast<int>(i);
+    if (idx < 0) throw std::invalid_argument("profile dnn '" + d.name() + "' is not in suite " + s.name);
+    if (s.nets[static_cast<std::size_t>(idx)].num_layers() != d.num_layers())
+      throw std::invalid_argument("profile dnn '" + d.name() + "' layer count differs from the network");
+    m.push_back(idx);
+  }
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bs_create(int device, const char* suite, int max_batch, int max_requests, bs_handle** out) {
+  return guarded([&] {
+    if (!suite || !out || max_batch < 1 || max_requests < 1) throw std::invalid_argument("bs_create: bad argument");
+    auto h = std::make_unique<bs_handle>();
+    h->ex = std::make_unique<Executor>(device, suite, max_batch, max_requests);
+    *out = h.release();
+    return BS_OK;
+  });
+}
+
+int bs_destroy(bs_handle* h) {
+  return guarded([&] {
+    delete h;
+    return BS_OK;
+  });
+}
+
+int bs_suite_json(bs_handle* h, char** out) {
+  return guarded([&] {
+    *out = dup_str(suite_json(h->ex->suite(), h->ex->blob_floats()).dump());
+    return BS_OK;
+  });
+}
+
+int bs_read_weights(bs_handle* h, float* dst, size_t n) {
+  return guarded([&] {
+    const auto& w = h->ex->suite().weights;
+    if (n < w.size()) throw std::invalid_argument("bs_read_weights: buffer too small");
+    std::memcpy(dst, w.data(), w.size() * sizeof(float));
+    return BS_OK;
+  });
+}
+
+int bs_make_image(uint64_t seed, uint64_t index, int H, int W, int C, int real_c, float* out) {
+  return guarded([&] {
+    synth_image(seed, index, H, W, C, real_c, out);
+    return BS_OK;
+  });
+}
+
+int bs_admit(bs_handle* h, int64_t id, int dnn, int entry_layer, const float* image_host) {
+  return guarded([&] {
+    h->ex->admit(id, dnn, entry_layer, image_host, false);
+    h->ex->sync();
+    return BS_OK;
+  });
+}
+
+int bs_plan(bs_handle* h, int plan_no) {
+  return guarded([&] {
+    h->ex->new_plan(plan_no);
+    return BS_OK;
+  });
+}
+
+int bs_step(bs_handle* h, int plan_no, int segment, int dnn, int layer_from, int layer_to, const bs_member* m, int nm,
+            const bs_rider* r, int nr) {
+  return guarded([&] {
+    std::vector<std::pair<std::int64_t, int>> members;
+    for (int i = 0; i < nm; ++i) members.emplace_back(m[i].id, m[i].layer);
+    std::vector<batchsim::Rider> riders;
+    for (int i = 0; i < nr; ++i)
+      riders.push_back({r[i].id, r[i].dnn, r[i].join_layer, r[i].leave_layer, r[i].deposit_layer});
+    h->ex->step(plan_no, segment, dnn, layer_from, layer_to, members, riders);
+    return BS_OK;
+  });
+}
+
+int bs_step_done(bs_handle* h, const int64_t* deposited, int n) {
+  return guarded([&] {
+    h->ex->step_done(std::vector<std::int64_t>(deposited, deposited + n));
+    return BS_OK;
+  });
+}
+
+int bs_retire(bs_handle* h, int64_t id, float* out, int n, int logits) {
+  return guarded([&] {
+    h->ex->retire(id, out, n, logits != 0);
+    return BS_OK;
+  });
+}
+
+int bs_drop(bs_handle* h, int64_t id) {
+  return guarded([&] {
+    h->ex->drop(id);
+    return BS_OK;
+  });
+}
+
+int bs_read_blob(bs_handle* h, int64_t id, float* dst, size_t n) {
+  return guarded([&] {
+    const float* b = h->ex->blob(id);
+    if (!b) throw std::logic_error("unknown request");
+    h->ex->sync();
+    const std::size_t cnt = std::min(n, h->ex->blob_floats());
+    if (cudaMemcpy(dst, b, cnt * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess)
+      throw std::runtime_error("blob copy failed");
+    return BS_OK;
+  });
+}
+
+int bs_sync(bs_handle* h) {
+  return guarded([&] {
+    h->ex->sync();
+    return BS_OK;
+  });
+}
+
+int bs_profile_layer(bs_handle* h, int dnn, int layer, int batch, int reps, int flush_l2, double* ms) {
+  return guarded([&] {
+    *ms = h->ex->profile_layer(dnn, layer, batch, reps, flush_l2 != 0);
+    return BS_OK;
+  });
+}
+
+int bs_replay(bs_handle* h, const char* job_json, char** out) {
+  return guarded([&] {
+    const json j = json::parse(job_json);
+    batchsim::SimJob job = batchsim::sim_job_from_json(j);
+    Executor& ex = *h->ex;
+    ReplayHook hook;
+    hook.ex = &ex;
+    hook.dnn_map = map_dnns(job.ps, ex.suite());
+    hook.image_seed = j.value("image_seed", std::uint64_t{1});
+    hook.pool = j.value("image_pool", 0) > 0;
+    if (hook.pool)
+      for (int net : hook.dnn_map) ex.make_image_pool(net, j.value("image_pool", 0), hook.image_seed);
+    for (const NetDef& n : ex.suite().nets) hook.classes = std::max(hook.classes, n.num_classes);
+    const std::size_t count = batchsim::generate_arrivals(job.spec).size();
+    float* results = nullptr;
+    if (cudaMallocHost(&results, std::max<std::size_t>(1, count) * hook.classes * sizeof(float)) != cudaSuccess)
+      throw std::runtime_error("pinned results");
+    std::memset(results, 0, count * hook.classes * sizeof(float));
+    hook.results = results;
+    const long launches0 = ex.launches();
+    const auto t0 = std::chrono::steady_clock::now();
+    batchsim::Simulator sim(job.spec, job.ps, job.config, job.trace ? &*job.trace : nullptr,
+                            job.client ? &*job.client : nullptr);
+    sim.set_hook(&hook);
+    batchsim::SimResult res;
+    try {
+      res = sim.run();
+      ex.sync();
+    } catch (...) {
+      cudaFreeHost(results);
+      throw;
+    }
+    const double wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::ostringstream os;
+    json outs = json::array();
+    for (const auto& o : res.outcomes) outs.push_back(batchsim::outcome_to_json(o));
+    os << json{{"ev", "outcomes"}, {"outcomes", outs}}.dump() << '\n';
+    json top1 = json::array();
+    for (std::size_t i = 0; i < count; ++i) {
+      const float* p = results + i * hook.classes;
+      int best = 0;
+      for (int c = 1; c < hook.classes; ++c)
+        if (p[c] > p[best]) best = c;
+      top1.push_back(p[best] > 0 ? best : -1);
+    }
+    json dumped = json::object();
+    for (const auto& idj : j.value("dump_ids", json::array())) {
+      const std::int64_t id = idj.get<std::int64_t>();
+      if (id >= 1 && static_cast<std::size_t>(id) <= count)
+        dumped[std::to_string(id)] =
+            std::vector<float>(results + (id - 1) * hook.classes, results + id * hook.classes);
+    }
+    cudaFreeHost(results);
+    json sm = batchsim::summary_to_json(res.metrics);
+    sm["wall_ms"] = wall_ms;
+    os << json{{"ev", "results"}, {"top1", top1}, {"probs", dumped}, {"launches", ex.launches() - launches0},
+               {"steps", hook.steps}, {"max_step_batch", hook.max_batch_seen}}
+              .dump()
+       << '\n';
+    os << sm.dump() << '\n';
+    *out = dup_str(os.str());
+    return BS_OK;
+  });
+}
+
+int bs_serve(bs_handle* h, const char* job_json, char** out) {
+  return guarded([&] {
+    *out = dup_str(serve_live(*h->ex, json::parse(job_json)).dump());
+    return BS_OK;
+  });
+}
+
+int bs_profile_table(bs_handle* h, const char* opts_json, char** out) {
+  return guarded([&] {
+    *out = dup_str(measure_profile(*h->ex, json::parse(opts_json)).dump());
+    return BS_OK;
+  });
+}
+
+void bs_free(char* p) { std::free(p); }
+
+}  // extern "C"

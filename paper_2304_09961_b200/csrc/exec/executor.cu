@@ -1,0 +1,462 @@
+#include "executor.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "../kernels/conv_tc.cuh"
+#include "../kernels/simple_ops.cuh"
+#include "bsb/core.hpp"
+#include "image.hpp"
+
+namespace bs200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kChunks = 64;
+
+}  // namespace
+
+Executor::Executor(int device, const std::string& suite_name, int max_batch, int max_requests)
+    : suite_(build_suite(suite_name)), device_(device), max_batch_(max_batch) {
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
+  ck(cudaMalloc(&d_weights_, suite_.weights.size() * sizeof(float)), "weights");
+  ck(cudaMemcpy(d_weights_, suite_.weights.data(), suite_.weights.size() * sizeof(float), cudaMemcpyHostToDevice),
+     "weights H2D");
+  for (const NetDef& n : suite_.nets) slot_floats_ = std::max<std::size_t>(slot_floats_, static_cast<std::size_t>(n.blob_floats));
+  slot_floats_ = (slot_floats_ + 63) / 64 * 64;
+  n_slots_ = max_requests;
+  ck(cudaMalloc(&arena_, static_cast<std::size_t>(n_slots_) * slot_floats_ * sizeof(float)), "arena");
+  for (int i = n_slots_ - 1; i >= 0; --i) free_.push_back(i);
+  n_ride_ = std::max(2 * max_batch_, 16);
+  ck(cudaMalloc(&ride_arena_, static_cast<std::size_t>(n_ride_) * slot_floats_ * sizeof(float)), "ride arena");
+  for (int i = n_ride_ - 1; i >= 0; --i) ride_free_.push_back(i);
+  int max_layers = 1;
+  for (const NetDef& n : suite_.nets) max_layers = std::max(max_layers, n.num_layers());
+  chunk_cap_ = static_cast<std::size_t>(max_layers) * static_cast<std::size_t>(max_batch_ + n_ride_) + 64;
+  chunks_.resize(kChunks);
+  for (auto& c : chunks_) {
+    ck(cudaMallocHost(&c.host, chunk_cap_ * sizeof(float*)), "pinned table");
+    ck(cudaMalloc(&c.dev, chunk_cap_ * sizeof(float*)), "device table");
+    ck(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming), "event");
+  }
+  // Scratch blobs for the profiler (max_batch of them) + an L2 flush buffer.
+  ck(cudaMalloc(&scratch_, static_cast<std::size_t>(max_batch_) * slot_floats_ * sizeof(float)), "scratch");
+  ck(cudaMemset(scratch_, 0, static_cast<std::size_t>(max_batch_) * slot_floats_ * sizeof(float)), "scratch zero");
+  ck(cudaMalloc(&scratch_ptrs_, max_batch_ * sizeof(float*)), "scratch ptrs");
+  std::vector<float*> hp(static_cast<std::size_t>(max_batch_));
+  for (int i = 0; i < max_batch_; ++i) hp[static_cast<std::size_t>(i)] = scratch_ + static_cast<std::size_t>(i) * slot_floats_;
+  ck(cudaMemcpy(scratch_ptrs_, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice), "scratch ptrs H2D");
+  pool_.assign(suite_.nets.size(), nullptr);
+  pool_n_.assign(suite_.nets.size(), 0);
+}
+
+Executor::~Executor() {
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  if (side_) cudaStreamSynchronize(side_);
+  for (auto& c : chunks_) {
+    cudaFreeHost(c.host);
+    cudaFree(c.dev);
+    cudaEventDestroy(c.done);
+  }
+  for (auto& [id, s] : slot_of_)
+    if (s.ready) cudaEventDestroy(s.ready);
+  for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+  for (auto& st : stats_) {
+    cudaEventDestroy(st.t0);
+    cudaEventDestroy(st.t1);
+  }
+  for (float* p : pool_) cudaFree(p);
+  cudaFree(d_weights_);
+  cudaFree(arena_);
+  cudaFree(ride_arena_);
+  cudaFree(scratch_);
+  cudaFree(scratch_ptrs_);
+  cudaFree(flush_);
+  cudaStreamDestroy(stream_);
+  cudaStreamDestroy(side_);
+}
+
+void Executor::sync() { ck(cudaStreamSynchronize(stream_), "sync"); }
+
+// ------------------------------------------------------------------ tables
+
+float** Executor::table_alloc(std::size_t n, float*** host_view) {
+  if (n > chunk_cap_) throw std::runtime_error("pointer table overflow");
+  if (chunk_used_ + n > chunk_cap_) throw std::runtime_error("pointer chunk overflow");
+  TableChunk& c = chunks_[chunk_];
+  *host_view = c.host + chunk_used_;
+  float** d = c.dev + chunk_used_;
+  chunk_used_ += n;
+  return d;
+}
+
+// ------------------------------------------------------------------ launch
+
+void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch) {
+  const auto off = [&](const TRef& r) -> long {
+    return r.t < 0 ? 0 : net.tensors[static_cast<std::size_t>(r.t)].off + r.coff;
+  };
+  const auto ldc = [&](const TRef& r) -> int { return r.t < 0 ? 0 : net.tensors[static_cast<std::size_t>(r.t)].C; };
+  const TensorDef& ti = net.tensors[static_cast<std::size_t>(op.in.t)];
+  LaunchStat st{};
+  if (stats_on_) {
+    st.kind = op.kind;
+    st.batch = batch;
+    st.bytes = op_bytes(net, op, batch);
+    st.flops = op_flops(op, batch);
+    ck(cudaEventCreate(&st.t0), "ev");
+    ck(cudaEventCreate(&st.t1), "ev");
+    ck(cudaEventRecord(st.t0, stream_), "ev rec");
+  }
+  cudaError_t e = cudaSuccess;
+  switch (op.kind) {
+    case OpKind::conv: {
+      ConvParams p{};
+      p.nimg = batch;
+      p.H = ti.H;
+      p.W = ti.W;
+      p.Cin = op.in.C;
+      p.Ho = op.Ho;
+      p.Wo = op.Wo;
+      p.KH = op.KH;
+      p.KW = op.KW;
+      p.stride = op.stride;
+      p.pad = op.pad;
+      p.K = op.KH * op.KW * op.in.C;
+      p.Kpad = op.Kpad;
+      p.N = op.out.C;
+      p.in_ptrs = d_ptrs;
+      p.in_off = off(op.in);
+      p.in_ldc = ldc(op.in);
+      p.wgt = d_weights_ + op.w_off;
+      p.bias = d_weights_ + op.b_off;
+      p.out_ptrs = d_ptrs;
+      p.out_off = off(op.out);
+      p.out_ldc = ldc(op.out);
+      p.res_ptrs = op.res.t >= 0 ? d_ptrs : nullptr;
+      p.res_off = off(op.res);
+      p.res_ldc = ldc(op.res);
+      p.relu = op.relu;
+      p.round_out = op.round_out;
+      e = launch_conv_tc(p, stream_);
+      break;
+    }
+    case OpKind::maxpool: {
+      PoolParams p{batch, ti.H, ti.W, op.in.C, op.Ho, op.Wo, op.KH, op.stride, op.pad,
+                   d_ptrs, off(op.in), ldc(op.in), d_ptrs, off(op.out), ldc(op.out)};
+      e = launch_maxpool(p, stream_);
+      break;
+    }
+    case OpKind::avgpool: {
+      AvgPoolParams p{batch, ti.H * ti.W, op.in.C, d_ptrs, off(op.in), ldc(op.in), d_ptrs, off(op.out), 1};
+      e = launch_avgpool(p, stream_);
+      break;
+    }
+    case OpKind::dwconv: {
+      DwParams p{batch, ti.H, ti.W, op.in.C, op.Ho, op.Wo, op.stride, d_ptrs, off(op.in), ldc(op.in),
+                 d_weights_ + op.w_off, d_weights_ + op.b_off, d_ptrs, off(op.out), ldc(op.out), op.relu,
+                 op.round_out};
+      e = launch_dwconv(p, stream_);
+      break;
+    }
+    case OpKind::softmax: {
+      SoftmaxParams p{batch, op.in.C, d_ptrs, off(op.in), off(op.out)};
+      e = launch_softmax(p, stream_);
+      break;
+    }
+  }
+  ck(e, op.name.c_str());
+  ++launches_;
+  if (stats_on_) {
+    ck(cudaEventRecord(st.t1, stream_), "ev rec");
+    stats_.push_back(st);
+  }
+}
+
+void Executor::run_layer(int dnn, int layer, float* const* d_ptrs, int batch) {
+  if (batch <= 0) return;
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
+  for (int oi : net.layers[static_cast<std::size_t>(layer - 1)].ops)
+    launch_op(net, net.ops[static_cast<std::size_t>(oi)], d_ptrs, batch);
+}
+
+// --------------------------------------------------------------- requests
+
+void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* image, bool on_device) {
+  if (slot_of_.count(id)) throw std::logic_error("request admitted twice: " + std::to_string(id));
+  if (free_.empty()) throw std::runtime_error("activation arena full");
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
+  Slot s;
+  s.index = free_.back();
+  free_.pop_back();
+  s.dnn = dnn;
+  s.blob = slot_ptr(s.index);
+  const TensorDef& in = net.tensors[static_cast<std::size_t>(net.input_t)];
+  const std::size_t bytes = static_cast<std::size_t>(in.H) * in.W * in.C * sizeof(float);
+  cudaStream_t st = entry_layer > 1 ? side_ : stream_;
+  ck(cudaMemcpyAsync(s.blob + in.off, image, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
+     "admit copy");
+  if (entry_layer > 1) {
+    // Collaborative mode: the client's layer prefix, emulated on a side
+    // stream so it stays off the server's critical path.
+    TableChunk& c = chunks_[chunk_];
+    (void)c;
+    float** host;
+    chunk_ = (chunk_ + 1) % chunks_.size();
+    TableChunk& mine = chunks_[chunk_];
+    if (mine.in_use) ck(cudaEventSynchronize(mine.done), "chunk wait");
+    chunk_used_ = 0;
+    float** d = table_alloc(1, &host);
+    host[0] = s.blob;
+    ck(cudaMemcpyAsync(d, host, sizeof(float*), cudaMemcpyHostToDevice, side_), "table H2D");
+    std::swap(stream_, side_);
+    try {
+      for (int k = 1; k < entry_layer; ++k) run_layer(dnn, k, d, 1);
+    } catch (...) {
+      std::swap(stream_, side_);
+      throw;
+    }
+    std::swap(stream_, side_);
+    ck(cudaEventRecord(mine.done, side_), "chunk done");
+    mine.in_use = true;
+    ck(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming), "ready ev");
+    ck(cudaEventRecord(s.ready, side_), "ready rec");
+    s.pending_ready = true;
+  }
+  slot_of_.emplace(id, s);
+}
+
+const float* Executor::blob(std::int64_t id) const {
+  auto it = slot_of_.find(id);
+  return it == slot_of_.end() ? nullptr : it->second.blob;
+}
+
+void Executor::retire(std::int64_t id, float* out, int n, bool logits) {
+  auto it = slot_of_.find(id);
+  if (it == slot_of_.end()) throw std::logic_error("retire of unknown request " + std::to_string(id));
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(it->second.dnn)];
+  const TensorDef& t = net.tensors[static_cast<std::size_t>(logits ? net.logits_t : net.probs_t)];
+  const int cnt = std::min(n, net.num_classes);
+  ck(cudaMemcpyAsync(out, it->second.blob + t.off, static_cast<std::size_t>(cnt) * sizeof(float),
+                     cudaMemcpyDeviceToHost, stream_),
+     "retire copy");
+  ck(cudaStreamSynchronize(stream_), "retire sync");
+  drop(id);
+}
+
+void Executor::retire_async(std::int64_t id, float* out, int n) {
+  auto it = slot_of_.find(id);
+  if (it == slot_of_.end()) throw std::logic_error("retire of unknown request " + std::to_string(id));
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(it->second.dnn)];
+  const TensorDef& t = net.tensors[static_cast<std::size_t>(net.probs_t)];
+  const int cnt = std::min(n, net.num_classes);
+  ck(cudaMemcpyAsync(out, it->second.blob + t.off, static_cast<std::size_t>(cnt) * sizeof(float),
+                     cudaMemcpyDeviceToHost, stream_),
+     "retire copy");
+  drop(id);  // slot reuse is stream-ordered after the copy
+}
+
+void Executor::drop(std::int64_t id) {
+  auto it = slot_of_.find(id);
+  if (it == slot_of_.end()) return;
+  if (it->second.ready) {
+    // a pending prefix must finish before the slot can be reused
+    ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
+    cudaEventDestroy(it->second.ready);
+  }
+  free_.push_back(it->second.index);
+  slot_of_.erase(it);
+  auto r = ride_of_.find(id);
+  if (r != ride_of_.end()) {
+    ride_free_.push_back(r->second);
+    ride_of_.erase(r);
+  }
+}
+
+// ------------------------------------------------------------------ steps
+
+void Executor::new_plan(int plan_no) {
+  // Rides in progress are discarded: the rider keeps its committed blob.
+  for (auto& [id, idx] : ride_of_) ride_free_.push_back(idx);
+  ride_of_.clear();
+  ride_plan_ = plan_no;
+}
+
+void Executor::step(int plan_no, int segment, int dnn, int from, int to,
+                    const std::vector<std::pair<std::int64_t, int>>& members,
+                    const std::vector<batchsim::Rider>& riders) {
+  if (plan_no != ride_plan_) new_plan(plan_no);
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
+  // Members whose prefix (collaborative entry) is still running.
+  for (const auto& [id, layer] : members) {
+    auto it = slot_of_.find(id);
+    if (it == slot_of_.end()) throw std::logic_error("step member not admitted: " + std::to_string(id));
+    if (it->second.pending_ready) {
+      ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
+      it->second.pending_ready = false;
+    }
+  }
+  // Members sorted by current layer: the batch at layer k is a prefix.
+  std::vector<std::pair<int, float*>> mem;
+  mem.reserve(members.size());
+  for (const auto& [id, layer] : members) mem.emplace_back(layer, slot_of_.at(id).blob);
+  std::stable_sort(mem.begin(), mem.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+
+  // Ride buffers for riders joining inside this step; riders that joined in
+  // an earlier step of the same plan continue on their buffer.
+  struct RideRun {
+    int join, leave;
+    float* buf;
+    float* committed;
+  };
+  std::vector<RideRun> rides;
+  for (const batchsim::Rider& r : riders) {
+    if (r.join_layer > to || r.leave_layer < from) continue;
+    auto it = slot_of_.find(r.id);
+    if (it == slot_of_.end()) continue;  // dropped meanwhile
+    auto rb = ride_of_.find(r.id);
+    float* buf;
+    if (rb == ride_of_.end()) {
+      if (ride_free_.empty()) throw std::runtime_error("ride arena full");
+      const int idx = ride_free_.back();
+      ride_free_.pop_back();
+      ride_of_[r.id] = idx;
+      buf = ride_arena_ + static_cast<std::size_t>(idx) * slot_floats_;
+    } else {
+      buf = ride_arena_ + static_cast<std::size_t>(rb->second) * slot_floats_;
+    }
+    rides.push_back({r.join_layer, r.leave_layer, buf, it->second.blob});
+  }
+
+  // One pointer chunk per step.
+  chunk_ = (chunk_ + 1) % chunks_.size();
+  TableChunk& c = chunks_[chunk_];
+  if (c.in_use) ck(cudaEventSynchronize(c.done), "chunk wait");
+  chunk_used_ = 0;
+  struct LayerRun {
+    int k;
+    float** d;
+    int b;
+  };
+  std::vector<LayerRun> runs;
+  std::vector<std::pair<int, RideRun>> copies;  // (layer before which to copy, ride)
+  std::size_t mi = 0;
+  for (int k = from; k <= to; ++k) {
+    while (mi < mem.size() && mem[mi].first <= k) ++mi;
+    int nr = 0;
+    for (const RideRun& rr : rides)
+      if (rr.join <= k && k <= rr.leave) ++nr;
+    const int b = static_cast<int>(mi) + nr;
+    if (b == 0) continue;
+    if (b > max_batch_) throw std::logic_error("step batch exceeds the configured bound");
+    float** host;
+    float** d = table_alloc(static_cast<std::size_t>(b), &host);
+    for (std::size_t i = 0; i < mi; ++i) host[i] = mem[i].second;
+    int j = static_cast<int>(mi);
+    for (const RideRun& rr : rides)
+      if (rr.join <= k && k <= rr.leave) host[j++] = rr.buf;
+    runs.push_back({k, d, b});
+  }
+  ck(cudaMemcpyAsync(c.dev, c.host, chunk_used_ * sizeof(float*), cudaMemcpyHostToDevice, stream_), "table H2D");
+  for (const LayerRun& lr : runs) {
+    for (const RideRun& rr : rides)
+      if (rr.join == lr.k)
+        ck(cudaMemcpyAsync(rr.buf, rr.committed, slot_floats_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_),
+           "ride copy");
+    run_layer(dnn, lr.k, lr.d, lr.b);
+  }
+  ck(cudaEventRecord(c.done, stream_), "chunk done");
+  c.in_use = true;
+  (void)net;
+  (void)segment;
+}
+
+void Executor::step_done(const std::vector<std::int64_t>& deposited) {
+  // Commit: the ride buffer becomes the rider's state (blob copy back so
+  // the slot keeps its fixed address).
+  for (std::int64_t id : deposited) {
+    auto rb = ride_of_.find(id);
+    auto it = slot_of_.find(id);
+    if (rb == ride_of_.end() || it == slot_of_.end()) continue;
+    ck(cudaMemcpyAsync(it->second.blob, ride_arena_ + static_cast<std::size_t>(rb->second) * slot_floats_,
+                       slot_floats_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_),
+       "ride commit");
+    ride_free_.push_back(rb->second);
+    ride_of_.erase(rb);
+  }
+}
+
+// -------------------------------------------------------------- measurement
+
+void Executor::enable_stats(bool on) { stats_on_ = on; }
+
+void Executor::clear_stats() {
+  for (auto& st : stats_) {
+    cudaEventDestroy(st.t0);
+    cudaEventDestroy(st.t1);
+  }
+  stats_.clear();
+}
+
+double Executor::profile_layer(int dnn, int layer, int batch, int reps, bool flush_l2) {
+  if (batch < 1 || batch > max_batch_) throw std::invalid_argument("profile batch out of range");
+  if (flush_l2 && !flush_) {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device_);
+    flush_bytes_ = static_cast<std::size_t>(std::max(l2, 1 << 20)) * 2;
+    ck(cudaMalloc(&flush_, flush_bytes_), "flush");
+  }
+  cudaEvent_t a, b;
+  ck(cudaEventCreate(&a), "ev");
+  ck(cudaEventCreate(&b), "ev");
+  std::vector<float> ms;
+  for (int r = -2; r < reps; ++r) {
+    if (flush_l2) ck(cudaMemsetAsync(flush_, r & 0xff, flush_bytes_, stream_), "flush");
+    ck(cudaEventRecord(a, stream_), "ev");
+    run_layer(dnn, layer, scratch_ptrs_, batch);
+    ck(cudaEventRecord(b, stream_), "ev");
+    ck(cudaEventSynchronize(b), "ev sync");
+    float t = 0;
+    ck(cudaEventElapsedTime(&t, a, b), "elapsed");
+    if (r >= 0) ms.push_back(t);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  std::sort(ms.begin(), ms.end());
+  return ms[ms.size() / 2];
+}
+
+// ------------------------------------------------------------- image pools
+
+void Executor::make_image_pool(int dnn, int count, std::uint64_t seed) {
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
+  const std::size_t per = static_cast<std::size_t>(net.in_H) * net.in_W * net.in_C;
+  std::vector<float> host(per * static_cast<std::size_t>(count));
+  for (int i = 0; i < count; ++i)
+    synth_image(seed, static_cast<std::uint64_t>(i), net.in_H, net.in_W, net.in_C, 3, host.data() + per * static_cast<std::size_t>(i));
+  if (pool_[static_cast<std::size_t>(dnn)]) cudaFree(pool_[static_cast<std::size_t>(dnn)]);
+  ck(cudaMalloc(&pool_[static_cast<std::size_t>(dnn)], host.size() * sizeof(float)), "image pool");
+  ck(cudaMemcpy(pool_[static_cast<std::size_t>(dnn)], host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice),
+     "image pool H2D");
+  pool_n_[static_cast<std::size_t>(dnn)] = count;
+}
+
+const float* Executor::pool_image(int dnn, int index) const {
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
+  const std::size_t per = static_cast<std::size_t>(net.in_H) * net.in_W * net.in_C;
+  return pool_[static_cast<std::size_t>(dnn)] + per * static_cast<std::size_t>(index % pool_n_[static_cast<std::size_t>(dnn)]);
+}
+
+int Executor::pool_size(int dnn) const { return pool_n_[static_cast<std::size_t>(dnn)]; }
+
+}  // namespace bs200

@@ -1,0 +1,145 @@
+// The B200 batched-layer executor.
+//
+//   * weights: one device pool per suite (TF32-rounded fp32), shared by every
+//     DNN that includes a component;
+//   * activation arena: one blob per admitted request (slot); a layer runs in
+//     place on its members' blobs; riders ride on a copy (ride buffer) that is
+//     committed only when the simulator deposits them (simulator.hpp:497-511
+//     "riders rewind");
+//   * a step = layers [from, to] of one DNN, layer k on {members with
+//     layer <= k} U {riders with join <= k <= leave} (simulator.hpp:705-713),
+//     all launched asynchronously on one stream; per-layer blob-pointer
+//     tables are uploaded once per step.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "bsb/schedulers.hpp"
+#include "netdef.hpp"
+
+namespace bs200 {
+
+struct LaunchStat {
+  OpKind kind;
+  int batch;
+  double bytes;   // algorithmic
+  double flops;
+  cudaEvent_t t0, t1;
+};
+
+struct RideKey {
+  std::int64_t id;
+  bool operator==(const RideKey& o) const { return id == o.id; }
+};
+
+class Executor {
+ public:
+  Executor(int device, const std::string& suite_name, int max_batch, int max_requests);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  const Suite& suite() const { return suite_; }
+  cudaStream_t stream() const { return stream_; }
+  int max_batch() const { return max_batch_; }
+
+  // ---- request lifecycle
+  // image: NHWC [in_H][in_W][in_C] floats, on host (copied H2D) or device.
+  void admit(std::int64_t id, int dnn, int entry_layer, const float* image, bool on_device);
+  void retire(std::int64_t id, float* probs_host, int n, bool logits = false);  // synchronous copy
+  void retire_async(std::int64_t id, float* probs_pinned, int n);               // stream-ordered copy + free
+  void drop(std::int64_t id);
+  bool has(std::int64_t id) const { return slot_of_.count(id) != 0; }
+  const float* blob(std::int64_t id) const;
+  std::size_t blob_floats() const { return slot_floats_; }
+  int free_slots() const { return static_cast<int>(free_.size()); }
+
+  // ---- batched step (async on stream())
+  void new_plan(int plan_no);
+  void step(int plan_no, int segment, int dnn, int from, int to,
+            const std::vector<std::pair<std::int64_t, int>>& members,
+            const std::vector<batchsim::Rider>& riders);
+  void step_done(const std::vector<std::int64_t>& deposited);
+
+  // Runs layers [from, to] of `dnn` on an explicit batch of blob pointers
+  // (the inner loop of step(); also used by the profiler).
+  void run_layer(int dnn, int layer, float* const* d_ptrs, int batch);
+
+  // ---- measurement
+  // Median of `reps` CUDA-event timings of one layer at batch b (cold L2 if
+  // flush), on scratch blobs.
+  double profile_layer(int dnn, int layer, int batch, int reps, bool flush_l2);
+  void enable_stats(bool on);
+  std::vector<LaunchStat>& stats() { return stats_; }
+  void clear_stats();
+  long launches() const { return launches_; }
+
+  void sync();
+
+  // Device-resident synthetic image pool (inputs resident in HBM for the
+  // bench); image i of dnn d.
+  void make_image_pool(int dnn, int count, std::uint64_t seed);
+  const float* pool_image(int dnn, int index) const;
+  int pool_size(int dnn) const;
+
+ private:
+  struct Slot {
+    int index = -1;
+    int dnn = 0;
+    float* blob = nullptr;
+    cudaEvent_t ready = nullptr;  // prefix (client-side layers) finished
+    bool pending_ready = false;
+  };
+  float* slot_ptr(int index) const { return arena_ + static_cast<std::size_t>(index) * slot_floats_; }
+  float** table_alloc(std::size_t n, float*** host_view);
+  void launch_op(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch);
+
+  Suite suite_;
+  int device_ = 0;
+  int max_batch_ = 90;
+  cudaStream_t stream_ = nullptr;
+  cudaStream_t side_ = nullptr;  // client-prefix emulation
+  float* d_weights_ = nullptr;
+  float* arena_ = nullptr;
+  std::size_t slot_floats_ = 0;
+  int n_slots_ = 0;
+  std::vector<int> free_;
+  std::unordered_map<std::int64_t, Slot> slot_of_;
+  // ride buffers: rider id -> ride slot index (valid for the current plan)
+  float* ride_arena_ = nullptr;
+  int n_ride_ = 0;
+  std::vector<int> ride_free_;
+  std::unordered_map<std::int64_t, int> ride_of_;
+  int ride_plan_ = -1;
+  // pointer tables: ring of pinned host + device chunks
+  struct TableChunk {
+    float** host = nullptr;
+    float** dev = nullptr;
+    cudaEvent_t done = nullptr;
+    bool in_use = false;
+  };
+  std::vector<TableChunk> chunks_;
+  std::size_t chunk_cap_ = 0;
+  std::size_t chunk_ = 0;
+  std::size_t chunk_used_ = 0;
+  // scratch for profiling
+  float* scratch_ = nullptr;
+  float** scratch_ptrs_ = nullptr;
+  float* flush_ = nullptr;
+  std::size_t flush_bytes_ = 0;
+  // image pools
+  std::vector<float*> pool_;
+  std::vector<int> pool_n_;
+  bool stats_on_ = false;
+  std::vector<LaunchStat> stats_;
+  std::vector<cudaEvent_t> event_pool_;
+  long launches_ = 0;
+};
+
+}  // namespace bs200

@@ -56,10 +56,10 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     p.H = d->H; p.W = d->W; p.Cin = d->Cin; p.Ho = d->Ho; p.Wo = d->Wo;
     p.KH = d->KH; p.KW = d->KW; p.stride = d->stride; p.pad = d->pad;
     p.K = K; p.Kpad = Kpad; p.N = d->N;
-    p.in_ptrs = ptrs; p.in_ldc = d->in_ldc; p.in_coff = d->in_coff;
+    p.in_ptrs = ptrs; p.in_ldc = d->in_ldc; p.in_off = d->in_coff;
     p.wgt = dw; p.bias = db;
-    p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_coff = d->out_coff;
-    p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_coff = d->res_coff;
+    p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_off = d->out_coff;
+    p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_off = d->res_coff;
     p.relu = d->relu; p.round_out = d->round_out;
     CK(launch_conv_tc(p, 0));
     CK(cudaDeviceSynchronize());

@@ -1,0 +1,363 @@
+#include "live.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstring>
+#include <deque>
+#include <stdexcept>
+#include <thread>
+
+#include "bsb/jobs.hpp"
+#include "image.hpp"
+
+using json = nlohmann::json;
+
+namespace bs200 {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+struct Book {
+  int dnn = 0;
+  double arrival = 0, deadline = 0, completion = -1;
+  bool dropped = false, done = false;
+};
+
+struct InFlight {
+  cudaEvent_t ev = nullptr;
+  double expected_end = 0;
+  std::vector<batchsim::RequestId> finishing;
+};
+
+}  // namespace
+
+json serve_live(Executor& ex, const json& j) {
+  using namespace batchsim;
+  SimJob job = sim_job_from_json(j);
+  const Suite& suite = ex.suite();
+  std::vector<int> dnn_map;
+  for (const auto& d : job.ps.dnns) {
+    int idx = -1;
+    for (std::size_t i = 0; i < suite.nets.size(); ++i)
+      if (suite.nets[i].name == d.name()) idx = static_cast<int>(i);
+    if (idx < 0 || suite.nets[static_cast<std::size_t>(idx)].num_layers() != d.num_layers())
+      throw std::invalid_argument("profile dnn '" + d.name() + "' does not match suite " + suite.name);
+    dnn_map.push_back(idx);
+  }
+  const int pool = j.value("image_pool", 32);
+  const bool h2d = j.value("h2d", false);
+  const std::uint64_t image_seed = j.value("image_seed", std::uint64_t{1});
+  const int depth = std::max(1, j.value("pipeline_depth", 2));
+  const bool deadlines = job.spec.relative_deadline < kNoDeadline;
+
+  // Inputs: device-resident pool (kernel-level runs) or pinned host images
+  // copied H2D at admission (end-to-end runs).
+  std::vector<float*> host_pool(suite.nets.size(), nullptr);
+  std::vector<std::size_t> img_floats(suite.nets.size(), 0);
+  for (std::size_t d = 0; d < dnn_map.size(); ++d) {
+    const int net = dnn_map[d];
+    const NetDef& nd = suite.nets[static_cast<std::size_t>(net)];
+    img_floats[static_cast<std::size_t>(net)] = static_cast<std::size_t>(nd.in_H) * nd.in_W * nd.in_C;
+    if (h2d) {
+      if (!host_pool[static_cast<std::size_t>(net)]) {
+        float* p = nullptr;
+        if (cudaMallocHost(&p, img_floats[static_cast<std::size_t>(net)] * pool * sizeof(float)) != cudaSuccess)
+          throw std::runtime_error("pinned image pool");
+        for (int i = 0; i < pool; ++i)
+          synth_image(image_seed, static_cast<std::uint64_t>(i), nd.in_H, nd.in_W, nd.in_C, 3,
+                      p + img_floats[static_cast<std::size_t>(net)] * static_cast<std::size_t>(i));
+        host_pool[static_cast<std::size_t>(net)] = p;
+      }
+    } else if (ex.pool_size(net) < pool) {
+      ex.make_image_pool(net, pool, image_seed);
+    }
+  }
+
+  const std::vector<ArrivalRecord> arrivals = generate_arrivals(job.spec);
+  const std::size_t n = arrivals.size();
+  std::vector<Book> book(n);
+  std::vector<int> mix;
+  if (job.spec.dnn_mix.empty()) {
+    mix.push_back(0);
+  } else {
+    for (const auto& m : job.spec.dnn_mix) mix.push_back(job.ps.dnn_index(m.first));
+  }
+  int classes = 0;
+  for (const NetDef& nd : suite.nets) classes = std::max(classes, nd.num_classes);
+  float* results = nullptr;
+  if (cudaMallocHost(&results, std::max<std::size_t>(n, 1) * classes * sizeof(float)) != cudaSuccess)
+    throw std::runtime_error("pinned results");
+
+  Planner planner(job.ps, job.config);
+  std::vector<Request> pending;
+  Schedule plan;
+  std::vector<detail::ExecStep> steps;
+  std::size_t next_step = 0;
+  int plan_no = 0;
+  bool needs_schedule = false;
+  int arrivals_since = 0;
+  std::deque<InFlight> inflight;
+  std::vector<cudaEvent_t> ev_free;
+  std::size_t ai = 0, resolved = 0;
+  long n_steps = 0, n_plans = 0, h2d_bytes = 0, d2h_bytes = 0;
+  double sched_ms = 0, max_sched_ms = 0;
+  const long launches0 = ex.launches();
+  std::vector<int> step_batch_hist;
+
+  auto finish = [&](RequestId id, double t) {
+    Book& b = book[static_cast<std::size_t>(id - 1)];
+    b.completion = t;
+    b.done = true;
+    ++resolved;
+  };
+  auto drop = [&](RequestId id) {
+    Book& b = book[static_cast<std::size_t>(id - 1)];
+    if (b.done || b.dropped) return;
+    b.dropped = true;
+    ++resolved;
+    ex.drop(id);
+  };
+  auto layer_shared = [&](int dnn, int layer) { return job.ps.layer_is_shared(dnn, layer); };
+
+  ex.sync();
+  const Clock::time_point t0 = Clock::now();
+  while (resolved < n) {
+    double now = ms_since(t0);
+    // 1. admissions
+    while (ai < n && arrivals[ai].time <= now) {
+      const RequestId id = static_cast<RequestId>(ai) + 1;
+      Book& b = book[ai];
+      b.dnn = mix[static_cast<std::size_t>(arrivals[ai].dnn) % mix.size()];
+      b.arrival = arrivals[ai].time;
+      b.deadline = deadlines ? arrivals[ai].time + job.spec.relative_deadline : kNoDeadline;
+      const int net = dnn_map[static_cast<std::size_t>(b.dnn)];
+      const int img = static_cast<int>(ai % static_cast<std::size_t>(pool));
+      if (h2d) {
+        ex.admit(id, net, 1, host_pool[static_cast<std::size_t>(net)] + img_floats[static_cast<std::size_t>(net)] * img,
+                 false);
+        h2d_bytes += static_cast<long>(img_floats[static_cast<std::size_t>(net)] * sizeof(float));
+      } else {
+        ex.admit(id, net, 1, ex.pool_image(net, img), true);
+      }
+      Request r;
+      r.id = id;
+      r.dnn = b.dnn;
+      r.arrival = b.arrival;
+      r.deadline = b.deadline;
+      r.layer = 1;
+      pending.insert(std::upper_bound(pending.begin(), pending.end(), r, arrives_before), r);
+      ++arrivals_since;
+      ++ai;
+    }
+    // 2. completions (in stream order)
+    while (!inflight.empty() && cudaEventQuery(inflight.front().ev) == cudaSuccess) {
+      now = ms_since(t0);
+      for (RequestId id : inflight.front().finishing) finish(id, now);
+      ev_free.push_back(inflight.front().ev);
+      inflight.pop_front();
+    }
+    // 3. plan + launch while the pipeline has room
+    if (static_cast<int>(inflight.size()) < depth && !pending.empty()) {
+      const double start_est = inflight.empty() ? now : std::max(now, inflight.back().expected_end);
+      if ((needs_schedule || next_step >= steps.size())) {
+        const auto s0 = Clock::now();
+        needs_schedule = false;
+        arrivals_since = 0;
+        next_step = 0;
+        steps.clear();
+        Planner::Result r = planner.plan(pending, start_est, deadlines);
+        for (RequestId id : r.dropped) drop(id);
+        if (r.computed) {
+          plan = std::move(r.plan);
+          steps = std::move(r.steps);
+          ++plan_no;
+          ++n_plans;
+          ex.new_plan(plan_no);
+        }
+        const double dt = std::chrono::duration<double, std::milli>(Clock::now() - s0).count();
+        sched_ms += dt;
+        max_sched_ms = std::max(max_sched_ms, dt);
+      }
+      if (next_step < steps.size()) {
+        const detail::ExecStep st = steps[next_step];
+        const ScheduledSegment& seg = plan.segments[static_cast<std::size_t>(st.segment)];
+        std::vector<std::pair<std::int64_t, int>> members;
+        for (RequestId id : seg.members)
+          for (const Request& r : pending)
+            if (r.id == id) {
+              members.emplace_back(id, r.layer);
+              break;
+            }
+        ex.step(plan_no, st.segment, dnn_map[static_cast<std::size_t>(seg.dnn)], st.layer_from, st.layer_to, members,
+                seg.riders);
+        ++n_steps;
+        // Effects apply at launch (the stream guarantees completion order);
+        // completion times are stamped when the step's event fires.
+        InFlight f;
+        bool crossed = false;
+        for (RequestId id : seg.members) {
+          auto it = std::find_if(pending.begin(), pending.end(), [id](const Request& r) { return r.id == id; });
+          if (it == pending.end() || it->layer > st.layer_to) continue;
+          const int was = it->layer;
+          it->layer = st.layer_to + 1;
+          const int nl = job.ps.dnns[static_cast<std::size_t>(it->dnn)].num_layers();
+          if (it->layer > nl) {
+            ex.retire_async(id, results + static_cast<std::size_t>(id - 1) * classes, classes);
+            d2h_bytes += classes * static_cast<long>(sizeof(float));
+            f.finishing.push_back(id);
+            pending.erase(it);
+          } else if (planner.has_shared() && layer_shared(it->dnn, was) != layer_shared(it->dnn, it->layer)) {
+            crossed = true;
+          }
+        }
+        std::vector<std::int64_t> deposited;
+        for (const Rider& rider : seg.riders) {
+          if (rider.leave_layer > st.layer_to || rider.join_layer > st.layer_to) continue;
+          auto it = std::find_if(pending.begin(), pending.end(), [&](const Request& r) { return r.id == rider.id; });
+          if (it == pending.end() || it->dnn != rider.dnn || it->layer >= rider.deposit_layer) continue;
+          it->layer = rider.deposit_layer;
+          crossed = true;
+          deposited.push_back(rider.id);
+        }
+        ex.step_done(deposited);
+        for (std::int64_t id : deposited) {
+          auto it = std::find_if(pending.begin(), pending.end(), [id](const Request& r) { return r.id == id; });
+          if (it != pending.end() && it->layer > job.ps.dnns[static_cast<std::size_t>(it->dnn)].num_layers()) {
+            ex.retire_async(id, results + static_cast<std::size_t>(id - 1) * classes, classes);
+            f.finishing.push_back(id);
+            pending.erase(it);
+          }
+        }
+        if (ev_free.empty()) {
+          cudaEvent_t e;
+          cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+          ev_free.push_back(e);
+        }
+        f.ev = ev_free.back();
+        ev_free.pop_back();
+        cudaEventRecord(f.ev, ex.stream());
+        f.expected_end = start_est + st.duration;
+        inflight.push_back(std::move(f));
+        ++next_step;
+        if (reschedule_trigger(true, arrivals_since > 0, crossed)) needs_schedule = true;
+        continue;
+      }
+    }
+    // 4. idle: wait for the next event
+    if (inflight.empty() && pending.empty() && ai < n) {
+      const double wait = arrivals[ai].time - ms_since(t0);
+      if (wait > 0.2) std::this_thread::sleep_for(std::chrono::microseconds(static_cast<long>((wait - 0.1) * 1000)));
+    }
+  }
+  ex.sync();
+  const double wall = ms_since(t0);
+  for (cudaEvent_t e : ev_free) cudaEventDestroy(e);
+
+  // Outcomes (reference semantics: drops count against on-time).
+  std::vector<RequestOutcome> outs(n);
+  double first_arrival = n ? arrivals.front().time : 0, last_completion = 0;
+  int on_time_completed = 0;
+  json top1 = json::array();
+  for (std::size_t i = 0; i < n; ++i) {
+    RequestOutcome& o = outs[i];
+    const Book& b = book[i];
+    o.id = static_cast<RequestId>(i) + 1;
+    o.dnn = b.dnn;
+    o.arrival = b.arrival;
+    o.deadline = b.deadline;
+    o.dropped = b.dropped;
+    if (b.done) {
+      o.completion = b.completion;
+      o.on_time = b.deadline >= kNoDeadline || b.completion <= b.deadline;
+      last_completion = std::max(last_completion, b.completion);
+      if (o.on_time) ++on_time_completed;
+      const float* p = results + i * classes;
+      int best = 0;
+      for (int c = 1; c < classes; ++c)
+        if (p[c] > p[best]) best = c;
+      top1.push_back(best);
+    } else {
+      top1.push_back(-1);
+    }
+  }
+  json dumped = json::object();
+  for (const auto& idj : j.value("dump_ids", json::array())) {
+    const std::int64_t id = idj.get<std::int64_t>();
+    if (id >= 1 && static_cast<std::size_t>(id) <= n && book[static_cast<std::size_t>(id - 1)].done)
+      dumped[std::to_string(id)] = std::vector<float>(results + (id - 1) * classes, results + id * classes);
+  }
+  cudaFreeHost(results);
+  for (float* p : host_pool)
+    if (p) cudaFreeHost(p);
+  const SummaryMetrics m = summarize(outs);
+  const double span_s = (last_completion - first_arrival) / 1000.0;
+  json out = summary_to_json(m);
+  out["on_time_ratio_f"] = m.on_time_ratio;
+  out["mean_completion_ms"] = m.mean_completion;
+  out["median_completion_ms"] = m.median_completion;
+  out["p95_completion_ms"] = m.p95_completion;
+  out["served_rps"] = span_s > 0 ? m.completed / span_s : 0.0;
+  out["goodput_rps"] = span_s > 0 ? on_time_completed / span_s : 0.0;
+  out["offered_rps"] = job.spec.rate;
+  out["wall_ms"] = wall;
+  out["span_ms"] = last_completion - first_arrival;
+  out["steps"] = n_steps;
+  out["plans"] = n_plans;
+  out["sched_ms_total"] = sched_ms;
+  out["sched_ms_max"] = max_sched_ms;
+  out["launches"] = ex.launches() - launches0;
+  out["h2d_bytes"] = h2d_bytes;
+  out["d2h_bytes"] = d2h_bytes;
+  out["top1"] = top1;
+  out["probs"] = dumped;
+  return out;
+}
+
+json measure_profile(Executor& ex, const json& opts) {
+  const Suite& s = ex.suite();
+  std::vector<int> batches = opts.value("batches", std::vector<int>{1, 2, 4, 8, 16, 32, 64, 90});
+  batches.erase(std::remove_if(batches.begin(), batches.end(), [&](int b) { return b < 1 || b > ex.max_batch(); }),
+                batches.end());
+  if (std::find(batches.begin(), batches.end(), 1) == batches.end()) batches.insert(batches.begin(), 1);
+  const int reps = opts.value("reps", 10);
+  const bool flush = opts.value("flush_l2", false);
+  json comps = json::array();
+  for (std::size_t c = 0; c < s.components.size(); ++c) {
+    // measure a component inside the first DNN that contains it
+    const NetDef* net = nullptr;
+    int net_idx = 0;
+    for (std::size_t i = 0; i < s.nets.size() && !net; ++i)
+      for (int cc : s.nets[i].components)
+        if (cc == static_cast<int>(c)) {
+          net = &s.nets[i];
+          net_idx = static_cast<int>(i);
+          break;
+        }
+    json layers = json::array();
+    for (int k = 1; k <= net->num_layers(); ++k) {
+      const LayerDef& L = net->layers[static_cast<std::size_t>(k - 1)];
+      if (L.component != static_cast<int>(c)) continue;
+      json grid = json::array();
+      for (int b : batches) grid.push_back(json::array({b, ex.profile_layer(net_idx, k, b, reps, flush)}));
+      const OpDef& last = net->ops[static_cast<std::size_t>(L.ops.back())];
+      const long bits = 32L * last.Ho * std::max(last.Wo, 1) * last.out.C;
+      layers.push_back({{"name", L.name}, {"output_bits", bits}, {"runtime_ms", grid}});
+    }
+    comps.push_back({{"id", s.components[c].id}, {"layers", layers}});
+  }
+  json dnns = json::array();
+  for (const NetDef& n : s.nets) {
+    json stages = json::array();
+    for (int c : n.components) stages.push_back(s.components[static_cast<std::size_t>(c)].id);
+    dnns.push_back({{"id", n.name}, {"stages", stages}});
+  }
+  return {{"max_batch", ex.max_batch()}, {"components", comps}, {"dnns", dnns}};
+}
+
+}  // namespace bs200

@@ -21,8 +21,7 @@
 #include <string>
 #include <typeinfo>
 
-#include "json_io.hpp"
-#include "server.hpp"
+#include "jobs.hpp"
 
 using json = nlohmann::json;
 using namespace batchsim;
@@ -31,70 +30,18 @@ namespace {
 
 thread_local std::string g_err;
 
-std::string hexbits(double v) {
-  std::uint64_t u;
-  std::memcpy(&u, &v, sizeof u);
-  char buf[24];
-  std::snprintf(buf, sizeof buf, "%016" PRIx64, u);
-  return buf;
-}
-
-double as_ms(const json& j) {
-  if (j.is_null()) return kNoDeadline;
-  if (j.is_string()) {
-    const std::string s = j.get<std::string>();
-    if (s == "inf") return kNoDeadline;
-    const std::uint64_t u = std::stoull(s, nullptr, 16);
-    double d;
-    std::memcpy(&d, &u, sizeof d);
-    return d;
-  }
-  return j.get<double>();
-}
-
-json to_json(const Schedule& s) {
-  json segs = json::array();
-  for (const auto& g : s.segments) {
-    json riders = json::array();
-    for (const auto& r : g.riders)
-      riders.push_back(json::array({r.id, r.dnn, r.join_layer, r.leave_layer, r.deposit_layer}));
-    segs.push_back({{"members", g.members},
-                    {"dnn", g.dnn},
-                    {"start_layer", g.start_layer},
-                    {"duration", hexbits(g.duration)},
-                    {"finish_offset", hexbits(g.finish_offset)},
-                    {"max_layer_batch", g.max_layer_batch},
-                    {"riders", riders}});
-  }
-  json offs = json::array();
-  for (const auto& [id, off] : s.completion_offsets) offs.push_back(json::array({id, hexbits(off)}));
-  return {{"segments", segs},
-          {"completion_offsets", offs},
-          {"objective", hexbits(s.objective)},
-          {"total_duration", hexbits(s.total_duration)},
-          {"tardy_count", s.tardy_count},
-          {"drop_marks", s.drop_marks}};
-}
-
 std::vector<Request> requests_of(const json& arr) {
   std::vector<Request> v;
   for (const auto& a : arr) {
     Request r;
     r.id = a.at(0).get<RequestId>();
     r.dnn = a.at(1).get<int>();
-    r.arrival = as_ms(a.at(2));
-    r.deadline = as_ms(a.at(3));
+    r.arrival = ms_from_json(a.at(2));
+    r.deadline = ms_from_json(a.at(3));
     r.layer = a.at(4).get<int>();
     v.push_back(r);
   }
   return v;
-}
-
-SplitGranularity granularity_of(const std::string& s) {
-  if (s == "request") return SplitGranularity::per_request;
-  if (s == "layer") return SplitGranularity::per_layer;
-  if (s == "group") return SplitGranularity::per_group;
-  throw std::invalid_argument("granularity " + s);
 }
 
 ProfileSet profile_of(const json& j) {
@@ -108,29 +55,29 @@ json one_call(const json& c, const ProfileSet& ps) {
   const int bound = c.value("bound", ps.max_batch);
   const int dnn = c.value("dnn", 0);
   DpOptions o;
-  o.granularity = granularity_of(c.value("granularity", std::string("request")));
+  o.granularity = granularity_from_name(c.value("granularity", std::string("request")));
   o.groups = c.value("groups", 5);
   o.extra_active = c.value("extra_active", 0);
-  const Ms now = c.contains("now") ? as_ms(c.at("now")) : 0.0;
+  const Ms now = c.contains("now") ? ms_from_json(c.at("now")) : 0.0;
   json out;
   try {
     if (fn == "dp") {
-      out["result"] = to_json(compute_schedule_dp(reqs, ps, dnn, bound, o));
+      out["result"] = schedule_to_json(compute_schedule_dp(reqs, ps, dnn, bound, o));
     } else if (fn == "tardy") {
-      const Ms off = c.contains("start_offset") ? as_ms(c.at("start_offset")) : 0.0;
-      out["result"] = to_json(tardy_dp(reqs, ps, dnn, bound, now, o, off));
+      const Ms off = c.contains("start_offset") ? ms_from_json(c.at("start_offset")) : 0.0;
+      out["result"] = schedule_to_json(tardy_dp(reqs, ps, dnn, bound, now, o, off));
     } else if (fn == "edf") {
-      out["result"] = to_json(edf_batch(reqs, ps, bound, now));
+      out["result"] = schedule_to_json(edf_batch(reqs, ps, bound, now));
     } else if (fn == "batch") {
-      out["result"] = to_json(baseline_batch(reqs, ps, bound));
+      out["result"] = schedule_to_json(baseline_batch(reqs, ps, bound));
     } else if (fn == "no_batch") {
-      out["result"] = to_json(baseline_no_batch(reqs, ps));
+      out["result"] = schedule_to_json(baseline_no_batch(reqs, ps));
     } else if (fn == "multi" || fn == "multi_shared") {
       MultiOptions mo;
       mo.dp = o;
       mo.permutation_guard = c.value("guard", 6);
       mo.allow_heuristic = c.value("heuristic", true);
-      out["result"] = to_json(fn == "multi" ? schedule_multi(reqs, ps, bound, mo)
+      out["result"] = schedule_to_json(fn == "multi" ? schedule_multi(reqs, ps, bound, mo)
                                             : schedule_multi_shared(reqs, ps, bound, mo));
     } else if (fn == "segment") {
       const std::vector<int> layers = c.at("layers").get<std::vector<int>>();
@@ -193,7 +140,7 @@ struct TraceWriter : SimObserver {
     if (!plans) return;
     json steps_j = json::array();
     for (const auto& s : st) steps_j.push_back(json::array({s.segment, s.layer_from, s.layer_to, hexbits(s.duration)}));
-    json p = to_json(plan);
+    json p = schedule_to_json(plan);
     p["ev"] = "plan";
     p["t"] = hexbits(now);
     p["n"] = plan_no;
@@ -210,81 +157,22 @@ struct TraceWriter : SimObserver {
 };
 
 void sim_job(const json& j, std::ostream& out) {
-  const ProfileSet ps = profile_of(j.at("profile"));
-  WorkloadSpec spec;
-  const json& w = j.at("workload");
-  spec.process = parse_process(w.value("process", std::string("poisson")));
-  spec.rate = w.value("rate", 100.0);
-  spec.count = w.value("count", 5000);
-  spec.pareto_alpha = w.value("pareto_alpha", 1.25);
-  if (w.contains("dnn_mix"))
-    for (const auto& m : w.at("dnn_mix")) spec.dnn_mix.emplace_back(m.at(0).get<std::string>(), m.at(1).get<double>());
-  spec.relative_deadline = w.contains("relative_deadline") ? as_ms(w.at("relative_deadline")) : kNoDeadline;
-  spec.seed = w.value("seed", std::uint64_t{1});
-  spec.size_lo_bits = w.value("size_lo_bits", std::int64_t{120000});
-  spec.size_hi_bits = w.value("size_hi_bits", std::int64_t{330000});
-  if (w.contains("size_trace")) spec.size_trace = w.at("size_trace").get<std::vector<std::int64_t>>();
-  if (w.contains("explicit_arrivals"))
-    for (const auto& a : w.at("explicit_arrivals"))
-      spec.explicit_arrivals.push_back({as_ms(a.at(0)), a.at(1).get<int>(), a.at(2).get<std::int64_t>()});
-  const json& s = j.at("sim");
-  SimConfig cfg;
-  cfg.scheduler = parse_scheduler(s.value("scheduler", std::string("ours-time")));
-  cfg.granularity = granularity_of(s.value("granularity", std::string("group")));
-  cfg.groups = s.value("groups", 5);
-  cfg.max_batch = s.value("max_batch", 90);
-  cfg.window_cap = s.value("window_cap", 500);
-  cfg.scheduler_latency = s.value("scheduler_latency", 0.0);
-  cfg.step_overhead = s.value("step_overhead", 0.0);
-  cfg.offload = parse_offload(s.value("offload", std::string("none")));
-  cfg.partial_rule = s.value("partial_rule", std::string("min_completion")) == "first_hide_wait"
-                         ? PartialRule::first_hide_wait
-                         : PartialRule::min_completion;
-  cfg.clients = s.value("clients", 0);
-  cfg.shared_batching = s.value("shared_batching", true);
-  std::optional<NetworkTrace> trace;
-  if (j.contains("trace")) {
-    NetworkTrace t = load_trace(j.at("trace").get<std::string>());
-    const double scale = j.value("trace_scale", 1.0);
-    trace = scale == 1.0 ? t : scale_trace(t, scale);
-  } else if (j.contains("trace_points")) {
-    std::vector<TracePoint> pts;
-    for (const auto& p : j.at("trace_points")) pts.push_back({as_ms(p.at(0)), as_ms(p.at(1))});
-    trace = NetworkTrace(std::move(pts));
-  }
-  std::optional<ClientProfile> client;
-  if (j.contains("client_profile")) client = load_client_profile(j.at("client_profile").get<std::string>());
-
+  SimJob job = sim_job_from_json(j);
   TraceWriter tw;
   tw.out = &out;
   tw.plans = j.value("emit_plans", true);
   tw.steps = j.value("emit_steps", true);
   const auto t0 = std::chrono::steady_clock::now();
-  Simulator sim(spec, ps, cfg, trace ? &*trace : nullptr, client ? &*client : nullptr);
+  Simulator sim(job.spec, job.ps, job.config, job.trace ? &*job.trace : nullptr, job.client ? &*job.client : nullptr);
   sim.set_observer(&tw);
   const SimResult res = sim.run();
   const double wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   json outs = json::array();
-  for (const auto& o : res.outcomes)
-    outs.push_back(json::array({o.id, o.dnn, hexbits(o.arrival), hexbits(o.completion), hexbits(o.deadline),
-                                o.on_time ? 1 : 0, o.dropped ? 1 : 0, static_cast<int>(o.location),
-                                o.offload_groups, hexbits(o.network_delay), hexbits(o.server_time),
-                                hexbits(o.client_time)}));
+  for (const auto& o : res.outcomes) outs.push_back(outcome_to_json(o));
   out << json{{"ev", "outcomes"}, {"outcomes", outs}}.dump() << '\n';
-  const auto& m = res.metrics;
-  out << json{{"ev", "summary"},
-              {"generated", m.generated},
-              {"completed", m.completed},
-              {"dropped", m.dropped},
-              {"on_time", m.on_time},
-              {"on_time_ratio", hexbits(m.on_time_ratio)},
-              {"mean_completion", hexbits(m.mean_completion)},
-              {"median_completion", hexbits(m.median_completion)},
-              {"p95_completion", hexbits(m.p95_completion)},
-              {"schedules_computed", m.schedules_computed},
-              {"wall_ms", wall_ms}}
-             .dump()
-      << '\n';
+  json sm = summary_to_json(res.metrics);
+  sm["wall_ms"] = wall_ms;
+  out << sm.dump() << '\n';
 }
 
 char* dup(const std::string& s) {

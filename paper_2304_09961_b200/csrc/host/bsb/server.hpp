@@ -102,6 +102,36 @@ struct StepHook {
   virtual void drop(RequestId id, Ms now) {}
 };
 
+// The reference's plan -> steps pipeline (simulator.hpp:541-721):
+// expiry drops, window cap, scheduler dispatch (incl. the Our-Tardy drop
+// loop), and the expansion of a schedule into executable steps with their
+// cost-table durations. Shared by the virtual-time Simulator and the live
+// wall-clock server so both make identical decisions on identical state.
+class Planner {
+ public:
+  Planner(const ProfileSet& ps, const SimConfig& config);
+  struct Result {
+    bool computed = false;  // false: the window emptied through expiry drops
+    Schedule plan;
+    std::vector<detail::ExecStep> steps;
+    std::vector<RequestId> dropped;  // expiry drops first, then tardy drops
+  };
+  Result plan(std::vector<Request>& pending, Ms now, bool deadlines);
+  Ms step_duration(const ScheduledSegment& seg, int from, int to, const std::vector<int>& layer_of) const;
+  bool has_shared() const { return has_shared_; }
+
+ private:
+  Schedule run_scheduler(std::vector<Request>& window, std::vector<Request>& pending, Ms now,
+                         std::vector<RequestId>& dropped);
+  Schedule tardy_multi(std::span<const Request> window, Ms now, const DpOptions& dp);
+  std::vector<detail::ExecStep> build_steps(const Schedule& plan, const std::vector<Request>& pending) const;
+
+  const ProfileSet& ps_;
+  SimConfig config_;
+  bool has_shared_ = false;
+  DpTable dp_cache_;
+};
+
 struct SimObserver {
   virtual ~SimObserver() = default;
   virtual void on_plan(Ms now, int plan_no, const Schedule& plan,
@@ -163,12 +193,6 @@ class Simulator {
   void end_of_instant(Ms now);
   void start_step(Ms now);
   void compute_plan(Ms now);
-  Schedule run_scheduler(std::vector<Request>& window, Ms now);
-  Schedule tardy_with_drops(std::vector<Request>& window, Ms now, const DpOptions& dp);
-  Schedule tardy_multi(std::span<const Request> window, Ms now, const DpOptions& dp);
-  void build_steps();
-  Ms step_duration(const ScheduledSegment& seg, int from, int to,
-                   const std::vector<int>& layer_of) const;
   std::int64_t payload_bits(const ClientDnnProfile& local, int dnn,
                             const std::vector<LayerGroup>& bounds, int k) const;
   void enqueue_client(int client, ClientJob job, Ms now);
@@ -191,6 +215,7 @@ class Simulator {
   SimConfig config_;
   const NetworkTrace* trace_;
   const ClientProfile* client_profile_;
+  Planner planner_;
   StepHook* hook_ = nullptr;
   SimObserver* obs_ = nullptr;
 
@@ -211,7 +236,6 @@ class Simulator {
   Ms plan_ready_at_ = 0;
   bool needs_schedule_ = false;
   int arrivals_since_schedule_ = 0;
-  DpTable dp_cache_;
   int schedules_computed_ = 0;
   double solve_wall_total_ = 0;
 };

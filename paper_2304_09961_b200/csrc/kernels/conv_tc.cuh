@@ -33,14 +33,17 @@ struct ConvParams {
   int K;                        // KH * KW * Cin
   int Kpad;                     // K rounded up to 32 (row stride of wgt)
   int N;                        // output channels
-  const float* const* in_ptrs;  // [nimg] image base pointers
-  int in_ldc, in_coff;          // floats per pixel, first channel
+  const float* const* in_ptrs;  // [nimg] per-request blob base pointers
+  long in_off;                  // element offset of (pixel 0, first channel) in the blob
+  int in_ldc;                   // floats per pixel
   const float* wgt;             // [N][Kpad], TF32-rounded, zero padded
   const float* bias;            // [N] or nullptr
   float* const* out_ptrs;       // [nimg]
-  int out_ldc, out_coff;
+  long out_off;
+  int out_ldc;
   const float* const* res_ptrs; // [nimg] or nullptr (residual add before ReLU)
-  int res_ldc, res_coff;
+  long res_off;
+  int res_ldc;
   int relu;                     // 0 none, 1 ReLU, 2 ReLU6
   int round_out;                // round outputs to TF32 (they feed another GEMM)
 };
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const ConvParams p
       const int wo = rem - ho * p.Wo;
       row_h[i] = ho * p.stride - p.pad;
       row_w[i] = wo * p.stride - p.pad;
-      row_base[i] = p.in_ptrs[n] + p.in_coff;
+      row_base[i] = p.in_ptrs[n] + p.in_off;
     }
     const uint32_t smem_base = ptx::smem_u32(smem);
     constexpr int kBRowsPerThread = BN / 16;
@@ -205,9 +208,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const ConvParams p
     }
     ptx::mbar_wait(accum_bar, 0);
     ptx::tc_fence_after();
-    float* out_row = m_ok ? p.out_ptrs[n_img] + static_cast<size_t>(pix) * p.out_ldc + p.out_coff : nullptr;
+    float* out_row = m_ok ? p.out_ptrs[n_img] + p.out_off + static_cast<size_t>(pix) * p.out_ldc : nullptr;
     const float* res_row = (m_ok && p.res_ptrs)
-                               ? p.res_ptrs[n_img] + static_cast<size_t>(pix) * p.res_ldc + p.res_coff
+                               ? p.res_ptrs[n_img] + p.res_off + static_cast<size_t>(pix) * p.res_ldc
                                : nullptr;
 #pragma unroll 1
     for (int j = 0; j < BN / 32; ++j) {

@@ -1,0 +1,57 @@
+// Bandwidth-bound NHWC ops on merged batches: max-pool, global average
+// pool, depthwise 3x3 conv, softmax. Every image has its own blob base
+// pointer (activation-arena slot) plus an element offset, exactly like the
+// tensor-core conv. Channels are processed four at a time (float4) so warps
+// issue 512-byte coalesced requests along the channel axis.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace bs200 {
+
+struct PoolParams {
+  int nimg, H, W, C, Ho, Wo;
+  int k, stride, pad;
+  const float* const* in_ptrs;
+  long in_off;
+  int in_ldc;
+  float* const* out_ptrs;
+  long out_off;
+  int out_ldc;
+};
+
+struct AvgPoolParams {
+  int nimg, HW, C;
+  const float* const* in_ptrs;
+  long in_off;
+  int in_ldc;
+  float* const* out_ptrs;
+  long out_off;
+  int round_out;
+};
+
+struct DwParams {
+  int nimg, H, W, C, Ho, Wo, stride;  // 3x3, pad 1
+  const float* const* in_ptrs;
+  long in_off;
+  int in_ldc;
+  const float* wgt;   // [9][C]
+  const float* bias;  // [C]
+  float* const* out_ptrs;
+  long out_off;
+  int out_ldc;
+  int relu;  // 0 none, 1 relu, 2 relu6
+  int round_out;
+};
+
+struct SoftmaxParams {
+  int nimg, N;
+  const float* const* ptrs;
+  long in_off, out_off;
+};
+
+cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s);
+cudaError_t launch_avgpool(const AvgPoolParams& p, cudaStream_t s);
+cudaError_t launch_dwconv(const DwParams& p, cudaStream_t s);
+cudaError_t launch_softmax(const SoftmaxParams& p, cudaStream_t s);
+
+}  // namespace bs200

@@ -1,0 +1,187 @@
+"""Python handle on libbs_exec.so (the B200 executor C-ABI, include/bs_exec.h).
+
+Mirrors the reference's serving entry points: admit / step / retire / drop
+at the points where batchsim's Simulator does arrive_at_server / start_step /
+finish / drop (proj/include/batchsim/simulator.hpp:447-751), plus replay
+(run_sim with every step executed), live serving and latency profiling.
+There is no CPU fallback: without the CUDA library or a GPU these raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+
+import numpy as np
+
+from ._native import BsError, FP, exec_lib
+
+_declared = False
+
+
+class bs_member(C.Structure):
+    _fields_ = [("id", C.c_int64), ("layer", C.c_int)]
+
+
+class bs_rider(C.Structure):
+    _fields_ = [("id", C.c_int64), ("dnn", C.c_int), ("join_layer", C.c_int),
+                ("leave_layer", C.c_int), ("deposit_layer", C.c_int)]
+
+
+def _lib():
+    global _declared
+    lib = exec_lib()
+    if not _declared:
+        H = C.c_void_p
+        sig = {
+            "bs_create": ([C.c_int, C.c_char_p, C.c_int, C.c_int, C.POINTER(H)], C.c_int),
+            "bs_destroy": ([H], C.c_int),
+            "bs_suite_json": ([H, C.POINTER(C.c_void_p)], C.c_int),
+            "bs_read_weights": ([H, FP, C.c_size_t], C.c_int),
+            "bs_make_image": ([C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, FP], C.c_int),
+            "bs_admit": ([H, C.c_int64, C.c_int, C.c_int, FP], C.c_int),
+            "bs_plan": ([H, C.c_int], C.c_int),
+            "bs_step": ([H, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(bs_member), C.c_int,
+                         C.POINTER(bs_rider), C.c_int], C.c_int),
+            "bs_step_done": ([H, C.POINTER(C.c_int64), C.c_int], C.c_int),
+            "bs_retire": ([H, C.c_int64, FP, C.c_int, C.c_int], C.c_int),
+            "bs_drop": ([H, C.c_int64], C.c_int),
+            "bs_read_blob": ([H, C.c_int64, FP, C.c_size_t], C.c_int),
+            "bs_sync": ([H], C.c_int),
+            "bs_profile_layer": ([H, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
+            "bs_profile_table": ([H, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
+            "bs_replay": ([H, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
+            "bs_serve": ([H, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
+            "bs_free": ([C.c_void_p], None),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = res
+        _declared = True
+    return lib
+
+
+def _check(rc):
+    if rc != 0:
+        msg = _lib().bs_last_error()
+        text = msg.decode() if msg else ""
+        if rc == -1:
+            raise ValueError(text)
+        if rc in (-4, -5):
+            raise RuntimeError(f"logic_error: {text}")
+        raise BsError(f"status {rc}: {text}")
+
+
+def _take_string(ptr: C.c_void_p) -> str:
+    try:
+        return C.string_at(ptr).decode()
+    finally:
+        _lib().bs_free(ptr)
+
+
+def make_image(seed: int, index: int, H: int, W: int, C_: int, real_c: int = 3) -> np.ndarray:
+    out = np.empty((H, W, C_), np.float32)
+    _check(_lib().bs_make_image(seed, index, H, W, C_, real_c, out.ctypes.data_as(FP)))
+    return out
+
+
+class Executor:
+    def __init__(self, suite: str, device: int = 0, max_batch: int = 90, max_requests: int = 1024):
+        h = C.c_void_p()
+        _check(_lib().bs_create(device, suite.encode(), max_batch, max_requests, C.byref(h)))
+        self._h = h
+        self.suite_name = suite
+        self.max_batch = max_batch
+        self._desc = None
+
+    def close(self):
+        if self._h:
+            _check(_lib().bs_destroy(self._h))
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- model
+    @property
+    def desc(self) -> dict:
+        if self._desc is None:
+            out = C.c_void_p()
+            _check(_lib().bs_suite_json(self._h, C.byref(out)))
+            self._desc = json.loads(_take_string(out))
+        return self._desc
+
+    def weights(self) -> np.ndarray:
+        w = np.empty(self.desc["weights"], np.float32)
+        _check(_lib().bs_read_weights(self._h, w.ctypes.data_as(FP), w.size))
+        return w
+
+    def dnn_index(self, name: str) -> int:
+        return [n["name"] for n in self.desc["nets"]].index(name)
+
+    # ------------------------------------------------------------- requests
+    def admit(self, rid: int, dnn: int, image: np.ndarray, entry_layer: int = 1):
+        image = np.ascontiguousarray(image, np.float32)
+        _check(_lib().bs_admit(self._h, rid, dnn, entry_layer, image.ctypes.data_as(FP)))
+
+    def plan(self, plan_no: int):
+        _check(_lib().bs_plan(self._h, plan_no))
+
+    def step(self, plan_no: int, segment: int, dnn: int, layer_from: int, layer_to: int,
+             members: list[tuple[int, int]], riders: list[tuple] = ()):
+        m = (bs_member * max(1, len(members)))(*[bs_member(i, l) for i, l in members])
+        r = (bs_rider * max(1, len(riders)))(*[bs_rider(*x) for x in riders])
+        _check(_lib().bs_step(self._h, plan_no, segment, dnn, layer_from, layer_to, m, len(members), r,
+                              len(riders)))
+
+    def step_done(self, deposited: list[int]):
+        arr = (C.c_int64 * max(1, len(deposited)))(*deposited)
+        _check(_lib().bs_step_done(self._h, arr, len(deposited)))
+
+    def retire(self, rid: int, n: int, logits: bool = False) -> np.ndarray:
+        out = np.empty(n, np.float32)
+        _check(_lib().bs_retire(self._h, rid, out.ctypes.data_as(FP), n, int(logits)))
+        return out
+
+    def drop(self, rid: int):
+        _check(_lib().bs_drop(self._h, rid))
+
+    def read_blob(self, rid: int) -> np.ndarray:
+        out = np.empty(self.desc["slot_floats"], np.float32)
+        _check(_lib().bs_read_blob(self._h, rid, out.ctypes.data_as(FP), out.size))
+        return out
+
+    def sync(self):
+        _check(_lib().bs_sync(self._h))
+
+    # ---------------------------------------------------------- measurement
+    def profile_layer(self, dnn: int, layer: int, batch: int, reps: int = 10, flush_l2: bool = False) -> float:
+        ms = C.c_double()
+        _check(_lib().bs_profile_layer(self._h, dnn, layer, batch, reps, int(flush_l2), C.byref(ms)))
+        return ms.value
+
+    def profile_table(self, batches=(1, 2, 4, 8, 16, 32, 64, 90), reps: int = 10, flush_l2: bool = False) -> dict:
+        out = C.c_void_p()
+        opts = json.dumps({"batches": list(batches), "reps": reps, "flush_l2": flush_l2})
+        _check(_lib().bs_profile_table(self._h, opts.encode(), C.byref(out)))
+        return json.loads(_take_string(out))
+
+    # -------------------------------------------------------------- serving
+    def replay(self, job: dict) -> list[dict]:
+        out = C.c_void_p()
+        _check(_lib().bs_replay(self._h, json.dumps(dict(job, job="sim")).encode(), C.byref(out)))
+        return [json.loads(l) for l in _take_string(out).splitlines()]
+
+    def serve(self, job: dict) -> dict:
+        out = C.c_void_p()
+        _check(_lib().bs_serve(self._h, json.dumps(dict(job, job="sim")).encode(), C.byref(out)))
+        return json.loads(_take_string(out))

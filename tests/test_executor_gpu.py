@@ -1,0 +1,183 @@
+"""Executor parity on the B200: layer outputs of merged batches (ragged
+membership, riders, rewinds, replayed schedules) against the CPU oracle.
+
+Tolerance (north_star): max|gpu - oracle| / max|oracle| <= 1e-3 per request
+on the final logits/probabilities, identical top-1. Per-layer blob checks use
+the same 1e-3 bound on every tensor the layer wrote.
+"""
+import numpy as np
+import pytest
+
+from oracle.forward import NetOracle, rel_err
+
+TOL = 1e-3
+pytestmark = pytest.mark.gpu
+
+
+def synth_profile(ex, base=1.0, slope=0.05):
+    """Reference-schema profile with the suite's layer structure (times are
+    synthetic; parity runs need only the structure)."""
+    d = ex.desc
+    comps = []
+    for c in d["components"]:
+        grid = [[b, base * (1 + slope * (b - 1))] for b in (1, 2, 4, 8, 16, 32, 64, 90) if b <= ex.max_batch]
+        if grid[-1][0] != ex.max_batch:
+            grid.append([ex.max_batch, base * (1 + slope * (ex.max_batch - 1))])
+        comps.append({"id": c["id"], "layers": [{"output_bits": 1000, "runtime_ms": grid}] * c["num_layers"]})
+    dnns = [{"id": n["name"], "stages": [d["components"][i]["id"] for i in n["components"]]} for n in d["nets"]]
+    return {"max_batch": ex.max_batch, "components": comps, "dnns": dnns}
+
+
+def image_for(ex, net, index, seed=1):
+    from paper_2304_09961_b200.executor import make_image
+    n = ex.desc["nets"][net]
+    return make_image(seed, index, n["in_H"], n["in_W"], n["in_C"])
+
+
+@pytest.fixture(scope="module")
+def googlenet():
+    from paper_2304_09961_b200.executor import Executor
+    ex = Executor("googlenet", max_batch=90, max_requests=64)
+    yield ex, ex.weights()
+    ex.close()
+
+
+def test_googlenet_ragged_steps_match_oracle(googlenet):
+    ex, w = googlenet
+    orc = NetOracle(ex.desc, 0, w)
+    imgs = {i: image_for(ex, 0, i) for i in (1, 2, 3)}
+    for i, img in imgs.items():
+        ex.admit(i, 0, img)
+    ex.plan(1)
+    ex.step(1, 0, 0, 1, 3, [(1, 1), (2, 1)])           # 1, 2 run layers 1-3
+    ex.step(1, 1, 0, 1, 5, [(3, 1), (1, 4), (2, 4)])   # 3 runs 1-5; 1, 2 join at 4
+    ref = {i: orc.forward(imgs[i], 1, 5) for i in imgs}
+    for i in imgs:
+        got = ex.read_blob(i)
+        for k in range(1, 6):
+            for oi in orc.d["layers"][k - 1]["ops"]:
+                op = orc.d["ops"][oi]
+                g = orc._view(got, op["out"])
+                r = orc._view(ref[i], op["out"])
+                assert rel_err(g, r) < TOL, (i, k, op["name"])
+    ex.step(1, 2, 0, 6, 22, [(1, 6), (2, 6), (3, 6)])
+    for i in imgs:
+        blob = orc.forward(imgs[i], 6, 22, blob=ref[i])
+        p_ref = orc.probs(blob)
+        l_ref = orc.logits(blob)
+        logits = ex.read_blob(i)[orc.d["tensors"][orc.d["logits"]]["off"]:][:1000]
+        assert rel_err(logits, l_ref) < TOL
+        p = ex.retire(i, 1000)
+        assert rel_err(p, p_ref) < TOL
+        assert int(np.argmax(p)) == int(np.argmax(p_ref))
+
+
+def test_googlenet_full_batch_90(googlenet):
+    ex, w = googlenet
+    orc = NetOracle(ex.desc, 0, w)
+    ids = list(range(100, 190))
+    for i in ids:
+        ex.admit(i, 0, image_for(ex, 0, i % 7))
+    ex.plan(2)
+    ex.step(2, 0, 0, 1, 22, [(i, 1) for i in ids])
+    probs = {i: ex.retire(i, 1000) for i in ids}
+    for j in range(3):  # spot-check distinct images
+        ref = orc.probs(orc.forward(image_for(ex, 0, j)))
+        for i in ids:
+            if i % 7 == j:
+                assert rel_err(probs[i], ref) < TOL
+                assert int(np.argmax(probs[i])) == int(np.argmax(ref))
+
+
+def test_small_cnn_replay_config1():
+    """Config 1: SmallCNN, Constant arrivals, completion-time DP, B = 10.
+    Schedules come from the bit-exact scheduler; every step executes."""
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("small_cnn", max_batch=10, max_requests=64) as ex:
+        w = ex.weights()
+        orc = NetOracle(ex.desc, 0, w)
+        prof = synth_profile(ex, 1.0, 0.02)
+        job = {"profile": prof, "workload": {"process": "constant", "rate": 900, "count": 40, "seed": 1},
+               "sim": {"scheduler": "ours-time", "granularity": "request", "max_batch": 10},
+               "image_seed": 7, "dump_ids": list(range(1, 41))}
+        out = ex.replay(job)
+        res = next(r for r in out if r["ev"] == "results")
+        summ = next(r for r in out if r["ev"] == "summary")
+        assert summ["completed"] == 40
+        assert res["max_step_batch"] > 1  # batching happened
+        for i in range(1, 41):
+            ref = orc.probs(orc.forward(image_for(ex, 0, i - 1, seed=7)))
+            got = np.array(res["probs"][str(i)], np.float32)[:10]
+            assert rel_err(got, ref) < TOL
+            assert res["top1"][i - 1] == int(np.argmax(ref))
+
+
+def test_resnet50_pair_riders_and_rewind():
+    """Config 3 mechanics: a foreign request rides the shared backbone inside
+    the other DNN's segment; an interrupted ride leaves it untouched."""
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("resnet50_pair", max_batch=90, max_requests=16) as ex:
+        w = ex.weights()
+        oa, ob = NetOracle(ex.desc, 0, w), NetOracle(ex.desc, 1, w)
+        ia, ib, ic = image_for(ex, 0, 0), image_for(ex, 1, 1), image_for(ex, 1, 2)
+        ex.admit(1, 0, ia)
+        ex.admit(2, 1, ib)
+        ex.admit(3, 1, ic)
+        # rewind: rider 3 rides layers 1-10 of a dnn-0 segment, then a new plan.
+        before = ex.read_blob(3)
+        ex.plan(1)
+        ex.step(1, 0, 0, 1, 10, [], [(3, 1, 1, 49, 50)])
+        ex.plan(2)
+        after = ex.read_blob(3)
+        assert np.array_equal(before, after)
+        # ride to the stage end and deposit
+        ex.step(2, 0, 0, 1, 49, [(1, 1)], [(2, 1, 1, 49, 50)])
+        ex.step_done([2])
+        ex.step(2, 0, 0, 50, 50, [(1, 50)])
+        ex.step(2, 1, 1, 50, 51, [(2, 50)])
+        pa, pb = ex.retire(1, 1000), ex.retire(2, 365)
+        ra = oa.probs(oa.forward(ia))
+        rb = ob.probs(ob.forward(ib))
+        assert rel_err(pa, ra) < TOL and int(np.argmax(pa)) == int(np.argmax(ra))
+        assert rel_err(pb, rb) < TOL and int(np.argmax(pb)) == int(np.argmax(rb))
+
+
+def test_mobilenet_v2_matches_oracle():
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("mobilenet_v2", max_batch=90, max_requests=8) as ex:
+        w = ex.weights()
+        orc = NetOracle(ex.desc, 0, w)
+        imgs = [image_for(ex, 0, i) for i in range(3)]
+        for i, img in enumerate(imgs):
+            ex.admit(i + 1, 0, img)
+        ex.plan(1)
+        ex.step(1, 0, 0, 1, 20, [(1, 1), (2, 1)])
+        ex.step(1, 1, 0, 1, 53, [(3, 1), (1, 21), (2, 21)])
+        for i, img in enumerate(imgs):
+            p = ex.retire(i + 1, 1000)
+            ref = orc.probs(orc.forward(img))
+            assert rel_err(p, ref) < TOL and int(np.argmax(p)) == int(np.argmax(ref))
+
+
+def test_profile_table_schema_loads_in_scheduler():
+    from paper_2304_09961_b200 import scheduler as bs
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("small_cnn", max_batch=10, max_requests=8) as ex:
+        prof = ex.profile_table(batches=(1, 2, 5, 10), reps=3)
+        assert len(prof["components"][0]["layers"]) == 5
+        assert all(ms > 0 for L in prof["components"][0]["layers"] for _, ms in L["runtime_ms"])
+        s = bs.compute_schedule([bs.make_request(1, 0.0, 1), bs.make_request(2, 0.0, 1)], prof, 0, 10)
+        assert s.objective > 0
+
+
+def test_live_serve_small():
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("googlenet", max_batch=90, max_requests=512) as ex:
+        prof = ex.profile_table(batches=(1, 8, 32, 90), reps=3)
+        t1 = sum(L["runtime_ms"][0][1] for L in prof["components"][0]["layers"])
+        job = {"profile": prof, "workload": {"process": "poisson", "rate": 2000, "count": 300, "seed": 3,
+                                             "relative_deadline": 20 * t1},
+               "sim": {"scheduler": "ours-tardy", "granularity": "layer"}, "image_pool": 16}
+        r = ex.serve(job)
+        assert r["completed"] + r["dropped"] == 300
+        assert r["completed"] > 0 and r["launches"] > 0
