@@ -20,7 +20,7 @@ class bs_conv_desc(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "H", "W", "Cin", "Ho", "Wo", "KH", "KW", "stride", "pad", "N",
         "in_ldc", "in_coff", "out_ldc", "out_coff", "res_ldc", "res_coff",
-        "relu", "round_out")]
+        "relu", "round_out", "split")]
 
 
 _exec = None

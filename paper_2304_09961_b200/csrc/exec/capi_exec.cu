@@ -160,6 +160,16 @@ int bs_suite_json(bs_handle* h, char** out) {
   });
 }
 
+int bs_describe_suite(const char* suite, char** out) {
+  return guarded([&] {
+    const Suite s = build_suite(suite);
+    std::size_t slot = 0;
+    for (const NetDef& n : s.nets) slot = std::max<std::size_t>(slot, static_cast<std::size_t>(n.blob_floats));
+    *out = dup_str(suite_json(s, slot).dump());
+    return BS_OK;
+  });
+}
+
 int bs_read_weights(bs_handle* h, float* dst, size_t n) {
   return guarded([&] {
     const auto& w = h->ex->suite().weights;
@@ -180,6 +190,13 @@ int bs_admit(bs_handle* h, int64_t id, int dnn, int entry_layer, const float* im
   return guarded([&] {
     h->ex->admit(id, dnn, entry_layer, image_host, false);
     h->ex->sync();
+    return BS_OK;
+  });
+}
+
+int bs_set_precision(bs_handle* h, const char* mode) {
+  return guarded([&] {
+    h->ex->set_precision(mode ? mode : "");
     return BS_OK;
   });
 }

@@ -57,6 +57,18 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   ck(cudaMemcpy(scratch_ptrs_, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice), "scratch ptrs H2D");
   pool_.assign(suite_.nets.size(), nullptr);
   pool_n_.assign(suite_.nets.size(), 0);
+  // One TMA descriptor per conv/FC weight matrix (weights never move).
+  wmaps_.resize(suite_.nets.size());
+  for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
+    const NetDef& net = suite_.nets[n];
+    wmaps_[n].resize(net.ops.size());
+    for (std::size_t i = 0; i < net.ops.size(); ++i) {
+      const OpDef& op = net.ops[i];
+      if (op.kind != OpKind::conv) continue;
+      if (!encode_weight_map(&wmaps_[n][i], d_weights_ + op.w_off, op.out.C, op.Kpad))
+        throw std::runtime_error("cuTensorMapEncodeTiled failed for " + op.name);
+    }
+  }
 }
 
 Executor::~Executor() {
@@ -87,6 +99,12 @@ Executor::~Executor() {
 }
 
 void Executor::sync() { ck(cudaStreamSynchronize(stream_), "sync"); }
+
+void Executor::set_precision(const std::string& mode) {
+  if (mode == "tf32x2") split_ = true;
+  else if (mode == "tf32") split_ = false;
+  else throw std::invalid_argument("unknown precision '" + mode + "' (tf32x2 | tf32)");
+}
 
 // ------------------------------------------------------------------ tables
 
@@ -122,6 +140,7 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
   switch (op.kind) {
     case OpKind::conv: {
       ConvParams p{};
+      p.wmap = wmaps_[static_cast<std::size_t>(&net - suite_.nets.data())][static_cast<std::size_t>(&op - net.ops.data())];
       p.nimg = batch;
       p.H = ti.H;
       p.W = ti.W;
@@ -147,7 +166,8 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
       p.res_off = off(op.res);
       p.res_ldc = ldc(op.res);
       p.relu = op.relu;
-      p.round_out = op.round_out;
+      p.round_out = split_ ? 0 : op.round_out;
+      p.split = split_ ? 1 : 0;
       e = launch_conv_tc(p, stream_);
       break;
     }
@@ -158,14 +178,14 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
       break;
     }
     case OpKind::avgpool: {
-      AvgPoolParams p{batch, ti.H * ti.W, op.in.C, d_ptrs, off(op.in), ldc(op.in), d_ptrs, off(op.out), 1};
+      AvgPoolParams p{batch, ti.H * ti.W, op.in.C, d_ptrs, off(op.in), ldc(op.in), d_ptrs, off(op.out), split_ ? 0 : 1};
       e = launch_avgpool(p, stream_);
       break;
     }
     case OpKind::dwconv: {
       DwParams p{batch, ti.H, ti.W, op.in.C, op.Ho, op.Wo, op.stride, d_ptrs, off(op.in), ldc(op.in),
                  d_weights_ + op.w_off, d_weights_ + op.b_off, d_ptrs, off(op.out), ldc(op.out), op.relu,
-                 op.round_out};
+                 split_ ? 0 : op.round_out};
       e = launch_dwconv(p, stream_);
       break;
     }

@@ -18,6 +18,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "bsb/schedulers.hpp"
@@ -82,6 +83,11 @@ class Executor {
 
   void sync();
 
+  // "tf32x2" (default): split-A 2xTF32 GEMMs, fp32 activations (fp32 parity);
+  // "tf32": one TF32 MMA per K step, activations rounded to TF32.
+  void set_precision(const std::string& mode);
+  const char* precision() const { return split_ ? "tf32x2" : "tf32"; }
+
   // Device-resident synthetic image pool (inputs resident in HBM for the
   // bench); image i of dnn d.
   void make_image_pool(int dnn, int count, std::uint64_t seed);
@@ -136,6 +142,8 @@ class Executor {
   // image pools
   std::vector<float*> pool_;
   std::vector<int> pool_n_;
+  std::vector<std::vector<CUtensorMap>> wmaps_;  // [net][op] weight tensor maps
+  bool split_ = true;
   bool stats_on_ = false;
   std::vector<LaunchStat> stats_;
   std::vector<cudaEvent_t> event_pool_;

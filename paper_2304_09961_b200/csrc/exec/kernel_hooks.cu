@@ -58,9 +58,13 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     p.K = K; p.Kpad = Kpad; p.N = d->N;
     p.in_ptrs = ptrs; p.in_ldc = d->in_ldc; p.in_off = d->in_coff;
     p.wgt = dw; p.bias = db;
+    if (!encode_weight_map(&p.wmap, dw, d->N, Kpad)) {
+      rc = bs_fail(BS_ECUDA, "cuTensorMapEncodeTiled failed");
+      goto done;
+    }
     p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_off = d->out_coff;
     p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_off = d->res_coff;
-    p.relu = d->relu; p.round_out = d->round_out;
+    p.relu = d->relu; p.round_out = d->round_out; p.split = d->split;
     CK(launch_conv_tc(p, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));

@@ -52,6 +52,8 @@ def _lib():
             "bs_replay": ([H, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
             "bs_serve": ([H, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
             "bs_free": ([C.c_void_p], None),
+            "bs_describe_suite": ([C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
+            "bs_set_precision": ([H, C.c_char_p], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -79,6 +81,13 @@ def _take_string(ptr: C.c_void_p) -> str:
         _lib().bs_free(ptr)
 
 
+def describe_suite(suite: str) -> dict:
+    """Network description of a suite, built on the host (no GPU needed)."""
+    out = C.c_void_p()
+    _check(_lib().bs_describe_suite(suite.encode(), C.byref(out)))
+    return json.loads(_take_string(out))
+
+
 def make_image(seed: int, index: int, H: int, W: int, C_: int, real_c: int = 3) -> np.ndarray:
     out = np.empty((H, W, C_), np.float32)
     _check(_lib().bs_make_image(seed, index, H, W, C_, real_c, out.ctypes.data_as(FP)))
@@ -93,6 +102,10 @@ class Executor:
         self.suite_name = suite
         self.max_batch = max_batch
         self._desc = None
+
+    def set_precision(self, mode: str):
+        """"tf32x2" (default, fp32 parity) or "tf32"."""
+        _check(_lib().bs_set_precision(self._h, mode.encode()))
 
     def close(self):
         if self._h:

@@ -37,7 +37,7 @@ def image_for(ex, net, index, seed=1):
 @pytest.fixture(scope="module")
 def googlenet():
     from paper_2304_09961_b200.executor import Executor
-    ex = Executor("googlenet", max_batch=90, max_requests=64)
+    ex = Executor("googlenet", max_batch=90, max_requests=128)
     yield ex, ex.weights()
     ex.close()
 

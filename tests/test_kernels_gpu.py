@@ -14,14 +14,16 @@ TOL = 2e-5
 
 
 def run_conv(nimg, H, W, Cin, N, KH, KW, stride, pad, *, in_ldc=None, in_coff=0, out_ldc=None,
-             out_coff=0, residual=False, relu=0, bias=True, seed=0, round_out=0):
+             out_coff=0, residual=False, relu=0, bias=True, seed=0, round_out=0, split=0, raw_input=False):
     from paper_2304_09961_b200._native import bs_conv_desc, check, exec_lib, fptr
     rng = np.random.default_rng(seed)
     in_ldc = in_ldc or Cin
     out_ldc = out_ldc or N
     Ho = (H + 2 * pad - KH) // stride + 1
     Wo = (W + 2 * pad - KW) // stride + 1
-    x_full = round_tf32(rng.standard_normal((nimg, H, W, in_ldc)).astype(np.float32))
+    x_full = rng.standard_normal((nimg, H, W, in_ldc)).astype(np.float32)
+    if not raw_input:
+        x_full = round_tf32(x_full)
     x = x_full[..., in_coff:in_coff + Cin]
     w = round_tf32((rng.standard_normal((N, KH, KW, Cin)) / np.sqrt(KH * KW * Cin)).astype(np.float32))
     K = KH * KW * Cin
@@ -42,7 +44,7 @@ def run_conv(nimg, H, W, Cin, N, KH, KW, stride, pad, *, in_ldc=None, in_coff=0,
 
     d = bs_conv_desc(H=H, W=W, Cin=Cin, Ho=Ho, Wo=Wo, KH=KH, KW=KW, stride=stride, pad=pad, N=N,
                      in_ldc=in_ldc, in_coff=in_coff, out_ldc=out_ldc, out_coff=out_coff,
-                     res_ldc=out_ldc, res_coff=out_coff, relu=relu, round_out=round_out)
+                     res_ldc=out_ldc, res_coff=out_coff, relu=relu, round_out=round_out, split=split)
     lib = exec_lib()
     check(lib.bs_kernel_conv(d, nimg, fptr(x_full), fptr(wp), fptr(b), fptr(res_full), fptr(out), 0,
                              None))
@@ -91,3 +93,17 @@ def test_conv_relu6():
 @pytest.mark.gpu
 def test_conv_large_batch():
     assert run_conv(90, 7, 7, 256, 256, 3, 3, 1, 1, bias=False) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES[:7], ids=lambda c: "x".join(str(c[k]) for k in ("nimg", "H", "Cin", "N", "KH", "stride")))
+def test_conv_split_tf32x2_full_fp32_inputs(case):
+    """2xTF32: un-rounded fp32 activations, TF32 weights -> fp32-level error."""
+    assert run_conv(**case, split=1, raw_input=True) < TOL
+
+
+@pytest.mark.gpu
+def test_conv_plain_tf32_on_fp32_inputs_is_worse():
+    """Sanity: without the split, un-rounded inputs lose ~1e-3 (the MMA truncates)."""
+    err = run_conv(2, 14, 14, 64, 128, 1, 1, 1, 0, raw_input=True)
+    assert 1e-5 < err < 5e-3
