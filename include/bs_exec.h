@@ -80,6 +80,8 @@ int bs_suite_json(bs_handle* h, char** out_json);
 int bs_read_weights(bs_handle* h, float* dst, size_t n);
 /* Same description without a device (builds the suite on the host only). */
 int bs_describe_suite(const char* suite, char** out_json);
+/* The suite's weight pool built on the host (no device). */
+int bs_suite_weights_host(const char* suite, float* dst, size_t n);
 /* The deterministic synthetic image for (seed, index). */
 int bs_make_image(uint64_t seed, uint64_t index, int H, int W, int C, int real_c, float* out);
 
@@ -101,6 +103,12 @@ int bs_sync(bs_handle* h);
 int bs_profile_layer(bs_handle* h, int dnn, int layer, int batch, int reps, int flush_l2, double* ms);
 /* opts: {"batches": [...], "reps": r, "flush_l2": bool} -> reference-schema profile JSON */
 int bs_profile_table(bs_handle* h, const char* opts_json, char** out_json);
+
+/* Sampled per-launch CUDA-event timing (every `every`-th launch). */
+int bs_stats(bs_handle* h, int enable, int every);
+/* JSON per kernel kind: launches, device ms, algorithmic bytes / FLOPs and
+ * the roofline-ideal time at the given HBM GB/s and tensor TFLOP/s. */
+int bs_stats_summary(bs_handle* h, double hbm_gbs, double tensor_tflops, char** out_json);
 
 /* ------------------------------------------------------------- serving */
 

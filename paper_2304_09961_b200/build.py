@@ -102,7 +102,7 @@ def build(verbose: bool = False) -> dict[str, Path]:
         out["host"] = host_so
     exec_so = LIB / "libbs_exec.so"
     _run([NVCC, "-shared", *GENCODE, "-o", str(exec_so), *map(str, exec_objs),
-          *map(str, host_objs), "-lcudart", "-lcuda"])
+          *map(str, host_objs), "-lcudart"])
     out["exec"] = exec_so
     if verbose:
         for k, v in out.items():

@@ -170,6 +170,15 @@ int bs_describe_suite(const char* suite, char** out) {
   });
 }
 
+int bs_suite_weights_host(const char* suite, float* dst, size_t n) {
+  return guarded([&] {
+    const Suite s = build_suite(suite);
+    if (n < s.weights.size()) throw std::invalid_argument("bs_suite_weights_host: buffer too small");
+    std::memcpy(dst, s.weights.data(), s.weights.size() * sizeof(float));
+    return BS_OK;
+  });
+}
+
 int bs_read_weights(bs_handle* h, float* dst, size_t n) {
   return guarded([&] {
     const auto& w = h->ex->suite().weights;
@@ -343,6 +352,47 @@ int bs_serve(bs_handle* h, const char* job_json, char** out) {
 int bs_profile_table(bs_handle* h, const char* opts_json, char** out) {
   return guarded([&] {
     *out = dup_str(measure_profile(*h->ex, json::parse(opts_json)).dump());
+    return BS_OK;
+  });
+}
+
+int bs_stats(bs_handle* h, int enable, int every) {
+  return guarded([&] {
+    h->ex->sync();
+    h->ex->clear_stats();
+    h->ex->enable_stats(enable != 0, every);
+    return BS_OK;
+  });
+}
+
+// Per-kind sums over the sampled launches: count, device ms, algorithmic
+// bytes and FLOPs, plus ideal time at the given peaks.
+int bs_stats_summary(bs_handle* h, double hbm_gbs, double tensor_tflops, char** out) {
+  return guarded([&] {
+    h->ex->sync();
+    json kinds = json::object();
+    for (const LaunchStat& st : h->ex->stats()) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, st.t0, st.t1) != cudaSuccess) continue;
+      const char* k = st.kind == OpKind::conv      ? "conv_tc"
+                      : st.kind == OpKind::maxpool ? "maxpool"
+                      : st.kind == OpKind::avgpool ? "avgpool"
+                      : st.kind == OpKind::dwconv  ? "dwconv"
+                                                   : "softmax";
+      json& e = kinds[k];
+      if (e.is_null()) e = {{"launches", 0}, {"ms", 0.0}, {"bytes", 0.0}, {"flops", 0.0}, {"ideal_ms", 0.0},
+                            {"ideal_hbm_ms", 0.0}, {"ideal_tensor_ms", 0.0}};
+      const double t_hbm = st.bytes / (hbm_gbs * 1e9) * 1e3;
+      const double t_tc = st.flops / (tensor_tflops * 1e12) * 1e3;
+      e["launches"] = e["launches"].get<int>() + 1;
+      e["ms"] = e["ms"].get<double>() + ms;
+      e["bytes"] = e["bytes"].get<double>() + st.bytes;
+      e["flops"] = e["flops"].get<double>() + st.flops;
+      e["ideal_ms"] = e["ideal_ms"].get<double>() + std::max(t_hbm, t_tc);
+      e["ideal_hbm_ms"] = e["ideal_hbm_ms"].get<double>() + t_hbm;
+      e["ideal_tensor_ms"] = e["ideal_tensor_ms"].get<double>() + t_tc;
+    }
+    *out = dup_str(kinds.dump());
     return BS_OK;
   });
 }

@@ -83,10 +83,6 @@ Executor::~Executor() {
   for (auto& [id, s] : slot_of_)
     if (s.ready) cudaEventDestroy(s.ready);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
-  for (auto& st : stats_) {
-    cudaEventDestroy(st.t0);
-    cudaEventDestroy(st.t1);
-  }
   for (float* p : pool_) cudaFree(p);
   cudaFree(d_weights_);
   cudaFree(arena_);
@@ -127,13 +123,14 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
   const auto ldc = [&](const TRef& r) -> int { return r.t < 0 ? 0 : net.tensors[static_cast<std::size_t>(r.t)].C; };
   const TensorDef& ti = net.tensors[static_cast<std::size_t>(op.in.t)];
   LaunchStat st{};
-  if (stats_on_) {
+  const bool sample = stats_on_ && (++stats_seen_ % stats_every_ == 0) && ev_next_ + 2 <= event_pool_.size();
+  if (sample) {
     st.kind = op.kind;
     st.batch = batch;
     st.bytes = op_bytes(net, op, batch);
     st.flops = op_flops(op, batch);
-    ck(cudaEventCreate(&st.t0), "ev");
-    ck(cudaEventCreate(&st.t1), "ev");
+    st.t0 = event_pool_[ev_next_++];
+    st.t1 = event_pool_[ev_next_++];
     ck(cudaEventRecord(st.t0, stream_), "ev rec");
   }
   cudaError_t e = cudaSuccess;
@@ -197,7 +194,7 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
   }
   ck(e, op.name.c_str());
   ++launches_;
-  if (stats_on_) {
+  if (sample) {
     ck(cudaEventRecord(st.t1, stream_), "ev rec");
     stats_.push_back(st);
   }
@@ -418,14 +415,18 @@ void Executor::step_done(const std::vector<std::int64_t>& deposited) {
 
 // -------------------------------------------------------------- measurement
 
-void Executor::enable_stats(bool on) { stats_on_ = on; }
+void Executor::enable_stats(bool on, int every) {
+  stats_on_ = on;
+  stats_every_ = std::max(1, every);
+  if (on && event_pool_.empty()) {
+    event_pool_.resize(1 << 16);
+    for (auto& e : event_pool_) ck(cudaEventCreate(&e), "event pool");
+  }
+}
 
 void Executor::clear_stats() {
-  for (auto& st : stats_) {
-    cudaEventDestroy(st.t0);
-    cudaEventDestroy(st.t1);
-  }
   stats_.clear();
+  ev_next_ = 0;
 }
 
 double Executor::profile_layer(int dnn, int layer, int batch, int reps, bool flush_l2) {

@@ -76,7 +76,9 @@ class Executor {
   // Median of `reps` CUDA-event timings of one layer at batch b (cold L2 if
   // flush), on scratch blobs.
   double profile_layer(int dnn, int layer, int batch, int reps, bool flush_l2);
-  void enable_stats(bool on);
+  // Sampled launch timing: every `every`-th conv launch (and every other
+  // kernel) gets an event pair from a preallocated pool.
+  void enable_stats(bool on, int every = 1);
   std::vector<LaunchStat>& stats() { return stats_; }
   void clear_stats();
   long launches() const { return launches_; }
@@ -145,6 +147,9 @@ class Executor {
   std::vector<std::vector<CUtensorMap>> wmaps_;  // [net][op] weight tensor maps
   bool split_ = true;
   bool stats_on_ = false;
+  int stats_every_ = 1;
+  long stats_seen_ = 0;
+  std::size_t ev_next_ = 0;
   std::vector<LaunchStat> stats_;
   std::vector<cudaEvent_t> event_pool_;
   long launches_ = 0;

@@ -1,6 +1,8 @@
 // Kernel-level C-ABI hooks: run one layer kernel on host buffers. Used by the
 // per-kernel parity tests (tests/test_kernels_gpu.py) and by the latency
 // profiler; the serving path goes through bs_step instead.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -65,9 +67,30 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_off = d->out_coff;
     p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_off = d->res_coff;
     p.relu = d->relu; p.round_out = d->round_out; p.split = d->split;
+    unsigned long long* trace = nullptr;
+    if (std::getenv("BS_CONV_TRACE")) {
+      CK(cudaMalloc(&trace, 8 * 300));
+      CK(cudaMemset(trace, 0, 8 * 300));
+      p.trace = trace;
+      CK(launch_conv_tc(p, 0));  // warm-up (TMEM/TMA descriptors, L2)
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemset(trace, 0, 8 * 300));
+    }
     CK(launch_conv_tc(p, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));
+    if (trace) {
+      unsigned long long h[300];
+      CK(cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost));
+      const unsigned long long t0 = h[0];
+      auto rel = [&](unsigned long long v) { return v ? static_cast<long long>(v - t0) : -1LL; };
+      std::fprintf(stderr, "trace: setup %lld epi %lld end %lld ns\n", rel(h[1]), rel(h[2]), rel(h[3]));
+      for (int kt = 0; kt < 64 && h[8 + 4 * kt]; ++kt)
+        std::fprintf(stderr, "  kt %2d A %7lld B %7lld mma %7lld split %7lld\n", kt, rel(h[8 + 4 * kt]),
+                     rel(h[9 + 4 * kt]), rel(h[10 + 4 * kt]), rel(h[11 + 4 * kt]));
+      p.trace = nullptr;
+      cudaFree(trace);
+    }
     if (reps > 0 && ms_per_launch) {
       CK(cudaEventCreate(&e0));
       CK(cudaEventCreate(&e1));

@@ -126,7 +126,11 @@ json serve_live(Executor& ex, const json& j) {
   auto layer_shared = [&](int dnn, int layer) { return job.ps.layer_is_shared(dnn, layer); };
 
   ex.sync();
+  cudaEvent_t dev0, dev1;
+  cudaEventCreate(&dev0);
+  cudaEventCreate(&dev1);
   const Clock::time_point t0 = Clock::now();
+  cudaEventRecord(dev0, ex.stream());
   while (resolved < n) {
     double now = ms_since(t0);
     // 1. admissions
@@ -255,8 +259,13 @@ json serve_live(Executor& ex, const json& j) {
       if (wait > 0.2) std::this_thread::sleep_for(std::chrono::microseconds(static_cast<long>((wait - 0.1) * 1000)));
     }
   }
+  cudaEventRecord(dev1, ex.stream());
   ex.sync();
   const double wall = ms_since(t0);
+  float device_ms = 0;
+  cudaEventElapsedTime(&device_ms, dev0, dev1);
+  cudaEventDestroy(dev0);
+  cudaEventDestroy(dev1);
   for (cudaEvent_t e : ev_free) cudaEventDestroy(e);
 
   // Outcomes (reference semantics: drops count against on-time).
@@ -306,6 +315,7 @@ json serve_live(Executor& ex, const json& j) {
   out["goodput_rps"] = span_s > 0 ? on_time_completed / span_s : 0.0;
   out["offered_rps"] = job.spec.rate;
   out["wall_ms"] = wall;
+  out["device_ms"] = device_ms;  // CUDA events on the serving stream, first admission to last retire
   out["span_ms"] = last_completion - first_arrival;
   out["steps"] = n_steps;
   out["plans"] = n_plans;

@@ -60,6 +60,7 @@ struct ConvParams {
   int relu;                     // 0 none, 1 ReLU, 2 ReLU6
   int round_out;                // round outputs to TF32 (they feed another GEMM)
   int split;                    // 1: 2xTF32 (A = A_hi + A_lo, near-fp32 accuracy)
+  unsigned long long* trace;    // debug timeline of CTA (0,0) (nullptr in production)
 };
 
 namespace conv_tc {
@@ -76,6 +77,18 @@ struct Smem {
   static constexpr int kBarOffset = STAGES * kStageBytes;
   static constexpr int kTotal = kBarOffset + 512 + 1024;  // barriers + alignment slack
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// trace layout: [0] start, [1] setup done, [2] epilogue start, [3] end,
+// [8 + 4 kt + {0: A issued, 1: B issued, 2: MMA got data, 3: split done}]
+#define BS_TRACE(slot)                                                         \
+  do {                                                                         \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0) p.trace[(slot)] = gtime(); \
+  } while (0)
 
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
@@ -102,6 +115,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
   const int n_base = blockIdx.y * BN;
   const int KT = p.Kpad / kBK;
   const uint32_t smem_base = ptx::smem_u32(smem);
+  if (threadIdx.x == 0) BS_TRACE(0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -118,6 +132,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) BS_TRACE(1);
 
   if (warp < 4) {
     // ------------------------------------------------------------ A gather
@@ -167,6 +182,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
             for (int i = 0; i < 8; ++i)
               ptx::cp_async16(a_tile + swz(r0 + 16 * i, c), ok[i] ? src[i] + ci : dummy, ok[i] ? 16u : 0u);
             ptx::cp_async_arrive_noinc(&raw_full[s]);
+            if (t == 0 && kt < 64) BS_TRACE(8 + 4 * kt);
           }
         }
       }
@@ -193,6 +209,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
           ptx::cp_async16(a_tile + swz(r0 + 16 * i, c), srcp, ok ? 16u : 0u);
         }
         ptx::cp_async_arrive_noinc(&raw_full[s]);
+        if (t == 0 && kt < 64) BS_TRACE(8 + 4 * kt);
       }
     }
   } else if (warp >= 8) {
@@ -217,6 +234,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&split_full[s]);
+        if (t == 0 && kt < 64) BS_TRACE(8 + 4 * kt + 3);
       }
     }
   } else {
@@ -227,6 +245,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         const int s = kt % STAGES;
         ptx::mbar_wait(&mma_full[s], (kt / STAGES) & 1);
         ptx::tc_fence_after();
+        if (lane == 0 && kt < 64) BS_TRACE(8 + 4 * kt + 2);
         if (lane == 0) {
           const uint32_t a_tile = smem_base + s * S::kStageBytes;
           const uint32_t b_tile = a_tile + S::kABytes * (SPLIT ? 2 : 1);
@@ -254,6 +273,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         const uint32_t b_tile = smem_base + s * S::kStageBytes + S::kABytes * (SPLIT ? 2 : 1);
         ptx::mbar_arrive_expect_tx(&raw_full[s], S::kBBytes);
         ptx::tma_load_2d(b_tile, &p.wmap, kt * kBK, n_base, &raw_full[s]);
+        if (kt < 64) BS_TRACE(8 + 4 * kt + 1);
       }
     }
     __syncwarp();
@@ -270,6 +290,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
     }
     ptx::mbar_wait(accum_bar, 0);
     ptx::tc_fence_after();
+    if (warp == 4 && lane == 0) BS_TRACE(2);
     float* out_row = m_ok ? p.out_ptrs[n_img] + p.out_off + static_cast<long>(pix) * p.out_ldc : nullptr;
     const float* res_row =
         (m_ok && p.res_ptrs) ? p.res_ptrs[n_img] + p.res_off + static_cast<long>(pix) * p.res_ldc : nullptr;
@@ -309,6 +330,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) BS_TRACE(3);
   if (warp == 4) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<BN>(tmem_base);

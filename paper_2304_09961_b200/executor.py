@@ -54,6 +54,8 @@ def _lib():
             "bs_free": ([C.c_void_p], None),
             "bs_describe_suite": ([C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
             "bs_set_precision": ([H, C.c_char_p], C.c_int),
+            "bs_stats": ([H, C.c_int, C.c_int], C.c_int),
+            "bs_stats_summary": ([H, C.c_double, C.c_double, C.POINTER(C.c_void_p)], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -186,6 +188,14 @@ class Executor:
         out = C.c_void_p()
         opts = json.dumps({"batches": list(batches), "reps": reps, "flush_l2": flush_l2})
         _check(_lib().bs_profile_table(self._h, opts.encode(), C.byref(out)))
+        return json.loads(_take_string(out))
+
+    def stats(self, enable: bool, every: int = 1):
+        _check(_lib().bs_stats(self._h, int(enable), every))
+
+    def stats_summary(self, hbm_gbs: float, tensor_tflops: float) -> dict:
+        out = C.c_void_p()
+        _check(_lib().bs_stats_summary(self._h, hbm_gbs, tensor_tflops, C.byref(out)))
         return json.loads(_take_string(out))
 
     # -------------------------------------------------------------- serving
