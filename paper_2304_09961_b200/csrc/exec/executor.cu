@@ -57,6 +57,11 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   ck(cudaMemcpy(scratch_ptrs_, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice), "scratch ptrs H2D");
   pool_.assign(suite_.nets.size(), nullptr);
   pool_n_.assign(suite_.nets.size(), 0);
+  conv_ws_.partial_floats = conv_workspace_floats();
+  conv_ws_.n_counters = conv_workspace_counters();
+  ck(cudaMalloc(&conv_ws_.partials, conv_ws_.partial_floats * sizeof(float)), "split-K workspace");
+  ck(cudaMalloc(&conv_ws_.counters, conv_ws_.n_counters * sizeof(int)), "split-K counters");
+  ck(cudaMemset(conv_ws_.counters, 0, conv_ws_.n_counters * sizeof(int)), "split-K counters zero");
   // One TMA descriptor per conv/FC weight matrix (weights never move).
   wmaps_.resize(suite_.nets.size());
   for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
@@ -84,6 +89,8 @@ Executor::~Executor() {
     if (s.ready) cudaEventDestroy(s.ready);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (float* p : pool_) cudaFree(p);
+  cudaFree(conv_ws_.partials);
+  cudaFree(conv_ws_.counters);
   cudaFree(d_weights_);
   cudaFree(arena_);
   cudaFree(ride_arena_);
@@ -165,7 +172,7 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
       p.relu = op.relu;
       p.round_out = split_ ? 0 : op.round_out;
       p.split = split_ ? 1 : 0;
-      e = launch_conv_tc(p, stream_);
+      e = launch_conv_tc(p, conv_ws_, stream_);
       break;
     }
     case OpKind::maxpool: {

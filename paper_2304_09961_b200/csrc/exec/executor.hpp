@@ -23,6 +23,7 @@
 
 #include "bsb/schedulers.hpp"
 #include "netdef.hpp"
+#include "../kernels/conv_tc.cuh"
 
 namespace bs200 {
 
@@ -145,6 +146,7 @@ class Executor {
   std::vector<float*> pool_;
   std::vector<int> pool_n_;
   std::vector<std::vector<CUtensorMap>> wmaps_;  // [net][op] weight tensor maps
+  ConvWorkspace conv_ws_;                         // split-K partials + tile counters
   bool split_ = true;
   bool stats_on_ = false;
   int stats_every_ = 1;

@@ -24,6 +24,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
   const size_t res_img = res_host ? static_cast<size_t>(d->Ho) * d->Wo * d->res_ldc : 0;
   float *din = nullptr, *dw = nullptr, *db = nullptr, *dout = nullptr, *dres = nullptr;
   float** ptrs = nullptr;
+  ConvWorkspace ws;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   int rc = BS_OK;
 #define CK(x)                                           \
@@ -41,6 +42,11 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     if (bias_host) CK(cudaMalloc(&db, d->N * sizeof(float)));
     if (res_host) CK(cudaMalloc(&dres, res_img * nimg * sizeof(float)));
     CK(cudaMalloc(&ptrs, 3 * nimg * sizeof(float*)));
+    ws.partial_floats = conv_workspace_floats();
+    ws.n_counters = conv_workspace_counters();
+    CK(cudaMalloc(&ws.partials, ws.partial_floats * sizeof(float)));
+    CK(cudaMalloc(&ws.counters, ws.n_counters * sizeof(int)));
+    CK(cudaMemset(ws.counters, 0, ws.n_counters * sizeof(int)));
     CK(cudaMemcpy(din, in_host, in_img * nimg * sizeof(float), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dw, w_host, static_cast<size_t>(d->N) * Kpad * sizeof(float), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dout, out_host, out_img * nimg * sizeof(float), cudaMemcpyHostToDevice));
@@ -69,25 +75,27 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     p.relu = d->relu; p.round_out = d->round_out; p.split = d->split;
     unsigned long long* trace = nullptr;
     if (std::getenv("BS_CONV_TRACE")) {
-      CK(cudaMalloc(&trace, 8 * 300));
-      CK(cudaMemset(trace, 0, 8 * 300));
+      CK(cudaMalloc(&trace, 8 * 1024));
+      CK(cudaMemset(trace, 0, 8 * 1024));
       p.trace = trace;
-      CK(launch_conv_tc(p, 0));  // warm-up (TMEM/TMA descriptors, L2)
+      CK(launch_conv_tc(p, ws, 0));  // warm-up (TMEM/TMA descriptors, L2)
       CK(cudaDeviceSynchronize());
-      CK(cudaMemset(trace, 0, 8 * 300));
+      CK(cudaMemset(trace, 0, 8 * 1024));
     }
-    CK(launch_conv_tc(p, 0));
+    CK(launch_conv_tc(p, ws, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));
     if (trace) {
-      unsigned long long h[300];
+      unsigned long long h[1024];
       CK(cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost));
-      const unsigned long long t0 = h[0];
+      unsigned long long t0 = ~0ULL;
+      for (int b = 0; b < 254; ++b)
+        if (h[8 + 4 * b] && h[8 + 4 * b] < t0) t0 = h[8 + 4 * b];
       auto rel = [&](unsigned long long v) { return v ? static_cast<long long>(v - t0) : -1LL; };
-      std::fprintf(stderr, "trace: setup %lld epi %lld end %lld ns\n", rel(h[1]), rel(h[2]), rel(h[3]));
-      for (int kt = 0; kt < 64 && h[8 + 4 * kt]; ++kt)
-        std::fprintf(stderr, "  kt %2d A %7lld B %7lld mma %7lld split %7lld\n", kt, rel(h[8 + 4 * kt]),
-                     rel(h[9 + 4 * kt]), rel(h[10 + 4 * kt]), rel(h[11 + 4 * kt]));
+      for (int b = 0; b < 254 && h[8 + 4 * b]; ++b)
+        if (b < 48 || b % 16 == 0)
+          std::fprintf(stderr, "  cta %3d start %7lld setup %7lld firstA %7lld end %7lld\n", b, rel(h[8 + 4 * b]),
+                       rel(h[9 + 4 * b]), rel(h[10 + 4 * b]), rel(h[11 + 4 * b]));
       p.trace = nullptr;
       cudaFree(trace);
     }
@@ -95,7 +103,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
       CK(cudaEventCreate(&e0));
       CK(cudaEventCreate(&e1));
       CK(cudaEventRecord(e0));
-      for (int r = 0; r < reps; ++r) CK(launch_conv_tc(p, 0));
+      for (int r = 0; r < reps; ++r) CK(launch_conv_tc(p, ws, 0));
       CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1));
       float ms = 0;
@@ -107,6 +115,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
 done:
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
+  cudaFree(ws.partials); cudaFree(ws.counters);
   cudaFree(din); cudaFree(dw); cudaFree(db); cudaFree(dout); cudaFree(dres); cudaFree(ptrs);
   return rc;
 }

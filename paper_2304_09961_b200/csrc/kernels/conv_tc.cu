@@ -1,11 +1,23 @@
 #include "conv_tc.cuh"
 
+#include <algorithm>
+
 namespace bs200 {
 
 namespace {
 
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
+    return v;
+  }();
+  return n;
+}
+
 template <int BN, int STAGES, bool SPLIT>
-cudaError_t launch_bn(const ConvParams& p, cudaStream_t stream) {
+cudaError_t launch_bn(const ConvParams& p, int grid, cudaStream_t stream) {
   using S = conv_tc::Smem<BN, STAGES, SPLIT>;
   static bool configured = false;
   if (!configured) {
@@ -14,8 +26,6 @@ cudaError_t launch_bn(const ConvParams& p, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int M = p.nimg * p.Ho * p.Wo;
-  dim3 grid((M + conv_tc::kBM - 1) / conv_tc::kBM, (p.N + BN - 1) / BN);
   conv_tc::conv_tc_kernel<BN, STAGES, SPLIT><<<grid, S::kThreads, S::kTotal, stream>>>(p);
   return cudaGetLastError();
 }
@@ -23,6 +33,9 @@ cudaError_t launch_bn(const ConvParams& p, cudaStream_t stream) {
 }  // namespace
 
 int conv_tile_n(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : 128; }
+
+std::size_t conv_workspace_floats() { return static_cast<std::size_t>(2 * 160) * conv_tc::kBM * 128; }
+int conv_workspace_counters() { return 2 * 2 * 160; }
 
 namespace {
 // The driver entry point is resolved through the runtime, so the library has
@@ -55,18 +68,54 @@ bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad) {
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_conv_tc(const ConvParams& p, cudaStream_t stream) {
+cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t stream) {
   if (p.Cin % 4 != 0 || p.Kpad % conv_tc::kBK != 0 || p.Kpad < p.K || p.nimg <= 0)
     return cudaErrorInvalidValue;
   const int bn = conv_tile_n(p.N);
-  if (p.split) {
-    if (bn == 32) return launch_bn<32, 4, true>(p, stream);
-    if (bn == 64) return launch_bn<64, 4, true>(p, stream);
-    return launch_bn<128, 4, true>(p, stream);
+  const int sms = sm_count();
+  const int KT = p.Kpad / conv_tc::kBK;
+  p.m_tiles = (p.nimg * p.Ho * p.Wo + conv_tc::kBM - 1) / conv_tc::kBM;
+  p.n_tiles = (p.N + bn - 1) / bn;
+  const int tiles = p.m_tiles * p.n_tiles;
+  // Split K when the tiles cannot cover the SMs (small merged batches).
+  // Pick the split count minimising the estimated makespan
+  //   waves(units) * (k tiles per unit + per-unit overhead),
+  // with every unit of a split-K launch co-resident (units <= SMs) so the
+  // cooperative reduction can wait on its tile's splits.
+  int ks = 1;
+  if (tiles < sms && ws.partials && ws.counters && 2 * tiles <= ws.n_counters) {
+    auto cost = [&](int k) {
+      const int per = (KT + k - 1) / k;
+      const int units = tiles * k;
+      const int waves = (units + sms - 1) / sms;
+      return waves * (per + (k > 1 ? 6 : 3));
+    };
+    int best = cost(1);
+    for (int k = 2; k <= 16 && tiles * k <= sms && k <= KT; ++k) {
+      if (static_cast<std::size_t>(tiles) * k * conv_tc::kBM * bn > ws.partial_floats) break;
+      const int c = cost(k);
+      if (c < best) {
+        best = c;
+        ks = k;
+      }
+    }
+    const int per = (KT + ks - 1) / ks;
+    ks = (KT + per - 1) / per;
   }
-  if (bn == 32) return launch_bn<32, 4, false>(p, stream);
-  if (bn == 64) return launch_bn<64, 4, false>(p, stream);
-  return launch_bn<128, 4, false>(p, stream);
+  p.ksplits = std::max(1, ks);
+  p.kt_per_split = (KT + p.ksplits - 1) / p.ksplits;
+  p.partials = ws.partials;
+  p.counters = ws.counters;
+  const int units = tiles * p.ksplits;
+  const int grid = std::min(units, sms);
+  if (p.split) {
+    if (bn == 32) return launch_bn<32, 4, true>(p, grid, stream);
+    if (bn == 64) return launch_bn<64, 4, true>(p, grid, stream);
+    return launch_bn<128, 4, true>(p, grid, stream);
+  }
+  if (bn == 32) return launch_bn<32, 6, false>(p, grid, stream);
+  if (bn == 64) return launch_bn<64, 6, false>(p, grid, stream);
+  return launch_bn<128, 6, false>(p, grid, stream);
 }
 
 }  // namespace bs200

@@ -4,30 +4,30 @@
 //   D[m, n] = sum_k A[m, k] * W[n, k]      m = (image, ho, wo), n = out channel,
 //                                          k = (kh, kw, ci) with ci fastest
 //
-// Mixed TMA / cp.async mainloop:
-//   * B (weights, a dense [N][Kpad] matrix) arrives by TMA, one 2D box per
-//     stage, 128B-swizzled — one instruction from one thread;
-//   * A is never materialised: producer warps gather 16-byte channel chunks of
-//     the NHWC input straight into 128B-swizzled shared memory with cp.async
-//     (zero-fill = spatial padding and M/K tails). Every image of the merged
-//     batch has its own base pointer, so requests stay in their own arena
-//     slots: the batch is "gathered" by the loader and "scattered" by the
-//     epilogue, with no copy kernels (gather/scatter row).
-//     Row addresses are computed once per filter tap (kh, kw); completion is
-//     signalled with cp.async.mbarrier.arrive.noinc, so producers never block
-//     on their own copies and the ring runs STAGES deep.
-//   * 2xTF32 split-A (default precision): the weights are exactly TF32 (they
-//     are generated that way), so A*W = A_hi*W + A_lo*W with A_hi = rn_tf32(A)
-//     recovers ~fp32 accuracy for two MMAs per K step and no extra HBM bytes.
-//     Splitter warps rewrite each landed A stage into [A_hi | A_lo].
+// Persistent, one CTA per SM. The launcher cuts the GEMM into work units =
+// (128 x BN output tile) x (K split); CTA c walks units c, c + G, c + 2G, ...
+// with one continuous shared-memory ring across units, so loads for the next
+// unit overlap the MMAs and epilogue of the current one. The accumulator is
+// double-buffered in TMEM (2 x BN columns): the epilogue of unit i drains one
+// buffer while the MMAs of unit i+1 fill the other. Small-M layers (batches
+// of a few requests) are split along K so the grid still covers all SMs;
+// partial tiles go to a workspace and the CTA that finishes a tile last
+// reduces them in fixed split order (deterministic results).
 //
-// Warp roles:
-//   warps 0-3   A producers (cp.async gather)
-//   warp  4     TMEM allocation; lane 0 issues tcgen05.mma
-//   warp  5     lane 0 issues the B TMA loads
-//   warps 4-7   epilogue: tcgen05.ld -> bias / residual / ReLU(6) / rounding
-//               -> per-image output slot (channel-slice writes = concat)
-//   warps 8-11  splitters (2xTF32 only)
+// Loads (mixed TMA / cp.async):
+//   * B (weights, dense [N][Kpad]) by TMA, one 128B-swizzled 2D box per stage;
+//   * A gathered straight from the NHWC request blobs with cp.async (zero-fill
+//     = spatial padding and M/K tails). Every image of a merged batch has its
+//     own base pointer, so requests stay in their own arena slots: the batch
+//     is gathered by the loader and scattered by the epilogue with no copy
+//     kernels. Completion: cp.async.mbarrier.arrive.noinc.
+//   * 2xTF32 split-A (default precision): weights are exactly TF32, so
+//     A*W = A_hi*W + A_lo*W with A_hi = rn_tf32(A) recovers ~fp32 accuracy at
+//     two MMAs per K step and no extra HBM traffic; splitter warps rewrite
+//     each landed A stage into [A_hi | A_lo].
+//
+// Warp roles: 0-3 A producers, 4-7 epilogue (TMEM lanes 0-127), 8 MMA issuer
+// (+ TMEM owner), 9 B TMA issuer, 10-13 splitters (2xTF32 only).
 #pragma once
 #include <cstdint>
 
@@ -60,7 +60,19 @@ struct ConvParams {
   int relu;                     // 0 none, 1 ReLU, 2 ReLU6
   int round_out;                // round outputs to TF32 (they feed another GEMM)
   int split;                    // 1: 2xTF32 (A = A_hi + A_lo, near-fp32 accuracy)
-  unsigned long long* trace;    // debug timeline of CTA (0,0) (nullptr in production)
+  // work decomposition (filled by launch_conv_tc)
+  int m_tiles, n_tiles, ksplits, kt_per_split;
+  float* partials;              // [units][128][BN] split-K workspace
+  int* counters;                // [tiles] zero between launches (reset by the reducer)
+  unsigned long long* trace;    // debug timeline of CTA 0 (nullptr in production)
+};
+
+// Device workspace for split-K (owned by the caller; counters zeroed once).
+struct ConvWorkspace {
+  float* partials = nullptr;
+  std::size_t partial_floats = 0;
+  int* counters = nullptr;
+  int n_counters = 0;
 };
 
 namespace conv_tc {
@@ -70,12 +82,12 @@ constexpr int kBK = 32;  // fp32 elements per 128-byte swizzle row
 
 template <int BN, int STAGES, bool SPLIT>
 struct Smem {
-  static constexpr int kThreads = SPLIT ? 384 : 256;
+  static constexpr int kThreads = SPLIT ? 448 : 320;
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kStageBytes = kABytes * (SPLIT ? 2 : 1) + kBBytes;  // [A_hi | A_lo | B]
   static constexpr int kBarOffset = STAGES * kStageBytes;
-  static constexpr int kTotal = kBarOffset + 512 + 1024;  // barriers + alignment slack
+  static constexpr int kTotal = kBarOffset + 1024 + 1024;  // barriers + alignment slack
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -83,15 +95,39 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// trace layout: [0] start, [1] setup done, [2] epilogue start, [3] end,
-// [8 + 4 kt + {0: A issued, 1: B issued, 2: MMA got data, 3: split done}]
-#define BS_TRACE(slot)                                                         \
-  do {                                                                         \
-    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0) p.trace[(slot)] = gtime(); \
-  } while (0)
 
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+struct Unit {
+  int m_base, n_base, tile, split, kt0, kt1;
+};
+
+__device__ __forceinline__ Unit unit_of(const ConvParams& p, int u, int BN, int KT) {
+  Unit w;
+  w.split = u % p.ksplits;
+  w.tile = u / p.ksplits;
+  const int mt = w.tile % p.m_tiles;  // consecutive tiles share a weight slice
+  const int nt = w.tile / p.m_tiles;
+  w.m_base = mt * kBM;
+  w.n_base = nt * BN;
+  w.kt0 = w.split * p.kt_per_split;
+  w.kt1 = min(KT, w.kt0 + p.kt_per_split);
+  return w;
+}
+
+__device__ __forceinline__ float epilogue_op(const ConvParams& p, float x, int n, const float* res_row) {
+  if (p.bias) x += __ldg(p.bias + n);
+  if (res_row) x += res_row[n];
+  if (p.relu == 1) x = fmaxf(x, 0.f);
+  else if (p.relu == 2) x = fminf(fmaxf(x, 0.f), 6.f);
+  if (p.round_out) x = ptx::round_tf32(x);
+  return x;
 }
 
 template <int BN, int STAGES, bool SPLIT>
@@ -104,18 +140,20 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
   uint64_t* split_full = raw_full + STAGES;
   uint64_t* empty_bar = split_full + STAGES;
-  uint64_t* accum_bar = empty_bar + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+  uint64_t* acc_full = empty_bar + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int* red_flag = reinterpret_cast<int*>(tmem_slot + 1);
   uint64_t* mma_full = SPLIT ? split_full : raw_full;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int M = p.nimg * p.Ho * p.Wo;
-  const int m_base = blockIdx.x * kBM;
-  const int n_base = blockIdx.y * BN;
   const int KT = p.Kpad / kBK;
+  const int units = p.m_tiles * p.n_tiles * p.ksplits;
   const uint32_t smem_base = ptx::smem_u32(smem);
-  if (threadIdx.x == 0) BS_TRACE(0);
+  // trace: [8 + 4 b + {0 start, 1 setup done, 2 first A issued, 3 end}]
+  if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x] = gtime();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -123,16 +161,19 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
       ptx::mbar_init(&split_full[s], 128);
       ptx::mbar_init(&empty_bar[s], 1);
     }
-    ptx::mbar_init(accum_bar, 1);
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&acc_full[a], 1);
+      ptx::mbar_init(&acc_empty[a], 128);
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 5 && lane == 0) ptx::prefetch_tmap(&p.wmap);
-  if (warp == 4) ptx::tmem_alloc<BN>(tmem_slot);
+  if (warp == 9 && lane == 0) ptx::prefetch_tmap(&p.wmap);
+  if (warp == 8) ptx::tmem_alloc<2 * BN>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) BS_TRACE(1);
+  if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x + 1] = gtime();
 
   if (warp < 4) {
     // ------------------------------------------------------------ A gather
@@ -140,113 +181,221 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
     const int c = t & 7;    // 16-byte chunk inside the 128-byte K row
     const int r0 = t >> 3;  // rows r0 + 16 i
     const int HoWo = p.Ho * p.Wo;
-    const float* row_base[8];
-    int row_h[8], row_w[8];
-    bool row_ok[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int m = m_base + r0 + 16 * i;
-      row_ok[i] = m < M;
-      const int mm = row_ok[i] ? m : 0;
-      const int n = mm / HoWo;
-      const int rem = mm - n * HoWo;
-      const int ho = rem / p.Wo;
-      const int wo = rem - ho * p.Wo;
-      row_h[i] = ho * p.stride - p.pad;
-      row_w[i] = wo * p.stride - p.pad;
-      row_base[i] = p.in_ptrs[n] + p.in_off;
-    }
     const float* dummy = p.wgt;
-    auto wait_slot = [&](int kt, int s) {
-      if (kt >= STAGES) ptx::mbar_wait(&empty_bar[s], ((kt / STAGES) - 1) & 1);
-    };
-    if (p.Cin % kBK == 0) {
-      // Filter-tap-major walk: row addresses once per (kh, kw), then the
-      // channel chunks are consecutive K tiles.
-      int kt = 0;
-      for (int kh = 0; kh < p.KH; ++kh) {
-        for (int kw = 0; kw < p.KW; ++kw) {
-          const float* src[8];
-          bool ok[8];
+    const bool aligned = p.Cin % kBK == 0;
+    int it = 0;  // ring position across units
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = unit_of(p, u, BN, KT);
+      const float* row_base[8];
+      int row_h[8], row_w[8];
+      bool row_ok[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int m = w.m_base + r0 + 16 * i;
+        row_ok[i] = m < M;
+        const int mm = row_ok[i] ? m : 0;
+        const int n = mm / HoWo;
+        const int rem = mm - n * HoWo;
+        const int ho = rem / p.Wo;
+        const int wo = rem - ho * p.Wo;
+        row_h[i] = ho * p.stride - p.pad;
+        row_w[i] = wo * p.stride - p.pad;
+        row_base[i] = p.in_ptrs[n] + p.in_off;
+      }
+      if (aligned) {
+        // Filter-tap-major walk: row addresses once per (kh, kw), channel
+        // chunks are consecutive K tiles.
+        int tap = (w.kt0 * kBK) / p.Cin;
+        int ci = w.kt0 * kBK - tap * p.Cin;
+        const float* src[8];
+        bool ok[8];
+        auto set_tap = [&] {
+          const int kh = tap / p.KW, kw = tap - (tap / p.KW) * p.KW;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int h = row_h[i] + kh, w = row_w[i] + kw;
-            ok[i] = row_ok[i] && h >= 0 && h < p.H && w >= 0 && w < p.W;
-            src[i] = ok[i] ? row_base[i] + (static_cast<long>(h) * p.W + w) * p.in_ldc + c * 4 : dummy;
+            const int h = row_h[i] + kh, ww = row_w[i] + kw;
+            ok[i] = row_ok[i] && h >= 0 && h < p.H && ww >= 0 && ww < p.W;
+            src[i] = ok[i] ? row_base[i] + (static_cast<long>(h) * p.W + ww) * p.in_ldc + c * 4 : dummy;
           }
-          for (int ci = 0; ci < p.Cin; ci += kBK, ++kt) {
-            const int s = kt % STAGES;
-            wait_slot(kt, s);
-            const uint32_t a_tile = smem_base + s * S::kStageBytes;
+        };
+        set_tap();
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) ptx::mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
+          const uint32_t a_tile = smem_base + s * S::kStageBytes;
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              ptx::cp_async16(a_tile + swz(r0 + 16 * i, c), ok[i] ? src[i] + ci : dummy, ok[i] ? 16u : 0u);
-            ptx::cp_async_arrive_noinc(&raw_full[s]);
-            if (t == 0 && kt < 64) BS_TRACE(8 + 4 * kt);
+          for (int i = 0; i < 8; ++i)
+            ptx::cp_async16(a_tile + swz(r0 + 16 * i, c), ok[i] ? src[i] + ci : dummy, ok[i] ? 16u : 0u);
+          ptx::cp_async_arrive_noinc(&raw_full[s]);
+          if (p.trace && t == 0 && it == 0) p.trace[8 + 4 * blockIdx.x + 2] = gtime();
+          ci += kBK;
+          if (ci == p.Cin && kt + 1 < w.kt1) {
+            ci = 0;
+            ++tap;
+            set_tap();
           }
         }
-      }
-    } else {
-      // Generic K decomposition (stem Cin = 4, narrow 1x1 inputs).
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % STAGES;
-        wait_slot(kt, s);
-        const uint32_t a_tile = smem_base + s * S::kStageBytes;
-        const int k0 = kt * kBK + c * 4;
-        const bool k_ok = k0 < p.K;
-        int ci = 0, kh = 0, kw = 0;
-        if (k_ok) {
-          const int q = k0 / p.Cin;
-          ci = k0 - q * p.Cin;
-          kh = q / p.KW;
-          kw = q - kh * p.KW;
-        }
+      } else {
+        // Generic K decomposition (stem Cin = 4, narrow 1x1 inputs).
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) ptx::mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
+          const uint32_t a_tile = smem_base + s * S::kStageBytes;
+          const int k0 = kt * kBK + c * 4;
+          const bool k_ok = k0 < p.K;
+          int ci = 0, kh = 0, kw = 0;
+          if (k_ok) {
+            const int q = k0 / p.Cin;
+            ci = k0 - q * p.Cin;
+            kh = q / p.KW;
+            kw = q - kh * p.KW;
+          }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int h = row_h[i] + kh, w = row_w[i] + kw;
-          const bool ok = k_ok && row_ok[i] && h >= 0 && h < p.H && w >= 0 && w < p.W;
-          const float* srcp = ok ? row_base[i] + (static_cast<long>(h) * p.W + w) * p.in_ldc + ci : dummy;
-          ptx::cp_async16(a_tile + swz(r0 + 16 * i, c), srcp, ok ? 16u : 0u);
+          for (int i = 0; i < 8; ++i) {
+            const int h = row_h[i] + kh, ww = row_w[i] + kw;
+            const bool ok = k_ok && row_ok[i] && h >= 0 && h < p.H && ww >= 0 && ww < p.W;
+            const float* srcp = ok ? row_base[i] + (static_cast<long>(h) * p.W + ww) * p.in_ldc + ci : dummy;
+            ptx::cp_async16(a_tile + swz(r0 + 16 * i, c), srcp, ok ? 16u : 0u);
+          }
+          ptx::cp_async_arrive_noinc(&raw_full[s]);
         }
-        ptx::cp_async_arrive_noinc(&raw_full[s]);
-        if (t == 0 && kt < 64) BS_TRACE(8 + 4 * kt);
       }
     }
-  } else if (warp >= 8) {
-    // --------------------------------------------------- 2xTF32 splitters
-    if constexpr (SPLIT) {
-      const int t = threadIdx.x - 256;
-      const int c = t & 7;
-      const int r0 = t >> 3;
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % STAGES;
-        ptx::mbar_wait(&raw_full[s], (kt / STAGES) & 1);
-        const uint32_t a_hi = smem_base + s * S::kStageBytes;
-        const uint32_t a_lo = a_hi + S::kABytes;
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;
+    const int et = threadIdx.x - 128;  // 0..127
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const Unit w = unit_of(p, u, BN, KT);
+      const int acc = j & 1;
+      ptx::mbar_wait(&acc_full[acc], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+      const int m = w.m_base + row;
+      const bool m_ok = m < M;
+      int n_img = 0, pix = 0;
+      if (m_ok) {
+        const int HoWo = p.Ho * p.Wo;
+        n_img = m / HoWo;
+        pix = m - n_img * HoWo;
+      }
+      float* out_row = m_ok ? p.out_ptrs[n_img] + p.out_off + static_cast<long>(pix) * p.out_ldc : nullptr;
+      const float* res_row =
+          (m_ok && p.res_ptrs) ? p.res_ptrs[n_img] + p.res_off + static_cast<long>(pix) * p.res_ldc : nullptr;
+      if (p.ksplits == 1) {
+#pragma unroll 1
+        for (int jj = 0; jj < BN / 32; ++jj) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + jj * 32, v);
+          ptx::tmem_ld_wait();
+          if (jj == BN / 32 - 1) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&acc_empty[acc]);  // TMEM buffer free for unit j + 2
+          }
+          const int n0 = w.n_base + jj * 32;
+          if (!m_ok || n0 >= p.N) continue;
+          const int ncols = min(32, p.N - n0);
+          float o[32];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t o = swz(r0 + 16 * i, c);
-          const float4 v = ptx::lds128(a_hi + o);
-          const float4 h = make_float4(ptx::round_tf32(v.x), ptx::round_tf32(v.y), ptx::round_tf32(v.z),
-                                       ptx::round_tf32(v.w));
-          ptx::sts128(a_hi + o, h);
-          ptx::sts128(a_lo + o, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
+          for (int q = 0; q < 32; ++q) o[q] = q < ncols ? epilogue_op(p, __uint_as_float(v[q]), n0 + q, res_row) : 0.f;
+          float* dst = out_row + n0;
+          if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+            for (int q = 0; q < 32; q += 4)
+              *reinterpret_cast<float4*>(dst + q) = make_float4(o[q], o[q + 1], o[q + 2], o[q + 3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q < ncols) dst[q] = o[q];
+          }
         }
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&split_full[s]);
-        if (t == 0 && kt < 64) BS_TRACE(8 + 4 * kt + 3);
+      } else {
+        // Split-K: park the raw partial tile; once all splits of the tile
+        // have landed (every unit of a split-K launch is co-resident: the
+        // launcher keeps units <= SMs), each split CTA reduces a slice of the
+        // tile rows in fixed split order (deterministic) and writes them.
+        float* part = p.partials + (static_cast<std::size_t>(u) * kBM + row) * BN;
+#pragma unroll 1
+        for (int jj = 0; jj < BN / 32; ++jj) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + jj * 32, v);
+          ptx::tmem_ld_wait();
+          if (jj == BN / 32 - 1) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&acc_empty[acc]);
+          }
+#pragma unroll
+          for (int q = 0; q < 32; q += 4)
+            __stcg(reinterpret_cast<float4*>(part + jj * 32 + q),
+                   make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]), __uint_as_float(v[q + 2]),
+                               __uint_as_float(v[q + 3])));
+        }
+        __threadfence();
+        named_bar(1, 128);
+        int* arrive = p.counters + 2 * w.tile;
+        if (et == 0) {
+          atomicAdd(arrive, 1);
+          while (atomicAdd(arrive, 0) < p.ksplits) __nanosleep(64);
+        }
+        named_bar(1, 128);
+        __threadfence();
+        // Rows [r_lo, r_hi) of this tile are reduced by this split.
+        const int rows_per = (kBM + p.ksplits - 1) / p.ksplits;
+        const int r_lo = w.split * rows_per, r_hi = min(kBM, r_lo + rows_per);
+        constexpr int kVec = BN / 4;  // float4 per row
+        const std::size_t first = static_cast<std::size_t>(w.tile) * p.ksplits;
+        for (int idx = et; idx < (r_hi - r_lo) * kVec; idx += 128) {
+          const int rr = r_lo + idx / kVec;
+          const int c4 = idx - (idx / kVec) * kVec;
+          const int mm = w.m_base + rr;
+          const int n0 = w.n_base + c4 * 4;
+          if (mm >= M || n0 >= p.N) continue;
+          float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int sp = 0; sp < p.ksplits; ++sp) {
+            const float4 x = __ldcg(reinterpret_cast<const float4*>(
+                p.partials + ((first + sp) * kBM + rr) * BN + c4 * 4));
+            acc4.x += x.x;
+            acc4.y += x.y;
+            acc4.z += x.z;
+            acc4.w += x.w;
+          }
+          const int HoWo = p.Ho * p.Wo;
+          const int img = mm / HoWo, px = mm - (mm / HoWo) * HoWo;
+          float* orow = p.out_ptrs[img] + p.out_off + static_cast<long>(px) * p.out_ldc;
+          const float* rrow = p.res_ptrs ? p.res_ptrs[img] + p.res_off + static_cast<long>(px) * p.res_ldc : nullptr;
+          const float vals[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (n0 + q < p.N) orow[n0 + q] = epilogue_op(p, vals[q], n0 + q, rrow);
+        }
+        // Last split out resets the tile's counters for the next launch.
+        named_bar(1, 128);
+        if (et == 0) {
+          __threadfence();
+          if (atomicAdd(p.counters + 2 * w.tile + 1, 1) == p.ksplits - 1) {
+            p.counters[2 * w.tile] = 0;
+            p.counters[2 * w.tile + 1] = 0;
+          }
+        }
       }
     }
-  } else {
-    if (warp == 4) {
-      // ---------------------------------------------------------- MMA issue
-      constexpr uint32_t idesc = ptx::make_idesc(2, kBM, BN);
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % STAGES;
-        ptx::mbar_wait(&mma_full[s], (kt / STAGES) & 1);
+  } else if (warp == 8) {
+    // ---------------------------------------------------------- MMA issue
+    constexpr uint32_t idesc = ptx::make_idesc(2, kBM, BN);
+    int it = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const Unit w = unit_of(p, u, BN, KT);
+      const int acc = j & 1;
+      if (j >= 2) ptx::mbar_wait(&acc_empty[acc], ((j >> 1) - 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+        const int s = it % STAGES;
+        ptx::mbar_wait(&mma_full[s], (it / STAGES) & 1);
         ptx::tc_fence_after();
-        if (lane == 0 && kt < 64) BS_TRACE(8 + 4 * kt + 2);
-        if (lane == 0) {
+        if (ptx::elect_one()) {
           const uint32_t a_tile = smem_base + s * S::kStageBytes;
           const uint32_t b_tile = a_tile + S::kABytes * (SPLIT ? 2 : 1);
           const uint64_t a_desc = ptx::sw128_kmajor_desc(a_tile);
@@ -254,86 +403,70 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 8; ++k) {
             // +32 bytes per K=8 step inside the swizzled row (>>4 -> +2).
-            ptx::mma_tf32(tmem_base, a_desc + 2 * k, b_desc + 2 * k, idesc, (kt | k) != 0);
+            ptx::mma_tf32(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
             if constexpr (SPLIT) {
               const uint64_t lo_desc = ptx::sw128_kmajor_desc(a_tile + S::kABytes);
-              ptx::mma_tf32(tmem_base, lo_desc + 2 * k, b_desc + 2 * k, idesc, 1);
+              ptx::mma_tf32(d_tmem, lo_desc + 2 * k, b_desc + 2 * k, idesc, 1);
             }
           }
           ptx::mma_commit(&empty_bar[s]);
-          if (kt == KT - 1) ptx::mma_commit(accum_bar);
+          if (kt == w.kt1 - 1) ptx::mma_commit(&acc_full[acc]);
         }
         __syncwarp();
       }
-    } else if (warp == 5 && lane == 0) {
-      // ------------------------------------------------------------ B TMA
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % STAGES;
-        if (kt >= STAGES) ptx::mbar_wait(&empty_bar[s], ((kt / STAGES) - 1) & 1);
-        const uint32_t b_tile = smem_base + s * S::kStageBytes + S::kABytes * (SPLIT ? 2 : 1);
-        ptx::mbar_arrive_expect_tx(&raw_full[s], S::kBBytes);
-        ptx::tma_load_2d(b_tile, &p.wmap, kt * kBK, n_base, &raw_full[s]);
-        if (kt < 64) BS_TRACE(8 + 4 * kt + 1);
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ B TMA
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = unit_of(p, u, BN, KT);
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) ptx::mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
+          const uint32_t b_tile = smem_base + s * S::kStageBytes + S::kABytes * (SPLIT ? 2 : 1);
+          ptx::mbar_arrive_expect_tx(&raw_full[s], S::kBBytes);
+          ptx::tma_load_2d(b_tile, &p.wmap, kt * kBK, w.n_base, &raw_full[s]);
+        }
       }
     }
     __syncwarp();
-    // ------------------------------------------------------------ epilogue
-    const int ew = warp - 4;
-    const int row = ew * 32 + lane;
-    const int m = m_base + row;
-    const bool m_ok = m < M;
-    int n_img = 0, pix = 0;
-    if (m_ok) {
-      const int HoWo = p.Ho * p.Wo;
-      n_img = m / HoWo;
-      pix = m - n_img * HoWo;
-    }
-    ptx::mbar_wait(accum_bar, 0);
-    ptx::tc_fence_after();
-    if (warp == 4 && lane == 0) BS_TRACE(2);
-    float* out_row = m_ok ? p.out_ptrs[n_img] + p.out_off + static_cast<long>(pix) * p.out_ldc : nullptr;
-    const float* res_row =
-        (m_ok && p.res_ptrs) ? p.res_ptrs[n_img] + p.res_off + static_cast<long>(pix) * p.res_ldc : nullptr;
-#pragma unroll 1
-    for (int j = 0; j < BN / 32; ++j) {
-      uint32_t v[32];
-      ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + j * 32, v);
-      ptx::tmem_ld_wait();
-      const int n0 = n_base + j * 32;
-      if (!m_ok || n0 >= p.N) continue;
-      const int ncols = min(32, p.N - n0);
-      float o[32];
+  } else {
+    // --------------------------------------------------- 2xTF32 splitters
+    if constexpr (SPLIT) {
+      const int t = threadIdx.x - 320;
+      const int c = t & 7;
+      const int r0 = t >> 3;
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = unit_of(p, u, BN, KT);
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+          const int s = it % STAGES;
+          ptx::mbar_wait(&raw_full[s], (it / STAGES) & 1);
+          const uint32_t a_hi = smem_base + s * S::kStageBytes;
+          const uint32_t a_lo = a_hi + S::kABytes;
 #pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        float x = __uint_as_float(v[q]);
-        if (q < ncols) {
-          if (p.bias) x += __ldg(p.bias + n0 + q);
-          if (res_row) x += res_row[n0 + q];
-          if (p.relu == 1) x = fmaxf(x, 0.f);
-          else if (p.relu == 2) x = fminf(fmaxf(x, 0.f), 6.f);
-          if (p.round_out) x = ptx::round_tf32(x);
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t o = swz(r0 + 16 * i, c);
+            const float4 v = ptx::lds128(a_hi + o);
+            const float4 h = make_float4(ptx::round_tf32(v.x), ptx::round_tf32(v.y), ptx::round_tf32(v.z),
+                                         ptx::round_tf32(v.w));
+            ptx::sts128(a_hi + o, h);
+            ptx::sts128(a_lo + o, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&split_full[s]);
         }
-        o[q] = x;
-      }
-      float* dst = out_row + n0;
-      if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-#pragma unroll
-        for (int q = 0; q < 32; q += 4)
-          *reinterpret_cast<float4*>(dst + q) = make_float4(o[q], o[q + 1], o[q + 2], o[q + 3]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q < ncols) dst[q] = o[q];
       }
     }
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) BS_TRACE(3);
-  if (warp == 4) {
+  if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x + 3] = gtime();
+  if (warp == 8) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<BN>(tmem_base);
+    ptx::tmem_dealloc<2 * BN>(tmem_base);
   }
 }
 
@@ -343,7 +476,11 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
 int conv_tile_n(int N);
 // Encodes a weight tensor map for w ([N][Kpad] floats) and the tile conv_tile_n(N).
 bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad);
-// Host-side launcher (p.wmap must be encoded for conv_tile_n(p.N)).
-cudaError_t launch_conv_tc(const ConvParams& p, cudaStream_t stream);
+// Host-side launcher: chooses the K split, grid and workspace use
+// (p.wmap must be encoded for conv_tile_n(p.N)).
+cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t stream);
+// Workspace sizing for the largest split-K decomposition the launcher uses.
+std::size_t conv_workspace_floats();
+int conv_workspace_counters();
 
 }  // namespace bs200
