@@ -75,27 +75,31 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     p.relu = d->relu; p.round_out = d->round_out; p.split = d->split;
     unsigned long long* trace = nullptr;
     if (std::getenv("BS_CONV_TRACE")) {
-      CK(cudaMalloc(&trace, 8 * 1024));
-      CK(cudaMemset(trace, 0, 8 * 1024));
+      CK(cudaMalloc(&trace, 8 * 1400));
+      CK(cudaMemset(trace, 0, 8 * 1400));
       p.trace = trace;
       CK(launch_conv_tc(p, ws, 0));  // warm-up (TMEM/TMA descriptors, L2)
       CK(cudaDeviceSynchronize());
-      CK(cudaMemset(trace, 0, 8 * 1024));
+      CK(cudaMemset(trace, 0, 8 * 1400));
     }
     CK(launch_conv_tc(p, ws, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));
     if (trace) {
-      unsigned long long h[1024];
+      unsigned long long h[1400];
       CK(cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost));
       unsigned long long t0 = ~0ULL;
       for (int b = 0; b < 254; ++b)
         if (h[8 + 4 * b] && h[8 + 4 * b] < t0) t0 = h[8 + 4 * b];
       auto rel = [&](unsigned long long v) { return v ? static_cast<long long>(v - t0) : -1LL; };
       for (int b = 0; b < 254 && h[8 + 4 * b]; ++b)
-        if (b < 48 || b % 16 == 0)
+        if (b < 2)
           std::fprintf(stderr, "  cta %3d start %7lld setup %7lld firstA %7lld end %7lld\n", b, rel(h[8 + 4 * b]),
                        rel(h[9 + 4 * b]), rel(h[10 + 4 * b]), rel(h[11 + 4 * b]));
+      for (int it = 0; it < 48 && h[1024 + it * 5 + 4]; ++it)
+        std::fprintf(stderr, "  it %2d A %7lld B %7lld landed %7lld split %7lld mma %7lld\n", it,
+                     rel(h[1024 + it * 5]), rel(h[1025 + it * 5]), rel(h[1026 + it * 5]), rel(h[1027 + it * 5]),
+                     rel(h[1028 + it * 5]));
       p.trace = nullptr;
       cudaFree(trace);
     }

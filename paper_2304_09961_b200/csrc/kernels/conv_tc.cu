@@ -1,6 +1,8 @@
 #include "conv_tc.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace bs200 {
 
@@ -108,6 +110,10 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   p.counters = ws.counters;
   const int units = tiles * p.ksplits;
   const int grid = std::min(units, sms);
+  static const bool log = std::getenv("BS_CONV_LOG") != nullptr;
+  if (log)
+    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d ws=%p\n", p.nimg * p.Ho * p.Wo, p.N,
+                 p.K, KT, bn, tiles, p.ksplits, grid, static_cast<void*>(ws.partials));
   if (p.split) {
     if (bn == 32) return launch_bn<32, 4, true>(p, grid, stream);
     if (bn == 64) return launch_bn<64, 4, true>(p, grid, stream);

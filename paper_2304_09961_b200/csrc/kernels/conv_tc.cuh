@@ -86,7 +86,8 @@ struct Smem {
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kStageBytes = kABytes * (SPLIT ? 2 : 1) + kBBytes;  // [A_hi | A_lo | B]
-  static constexpr int kBarOffset = STAGES * kStageBytes;
+  static constexpr int kStagingOffset = STAGES * kStageBytes;  // epilogue staging, 128 x 32 fp32
+  static constexpr int kBarOffset = kStagingOffset + kBM * 32 * 4;
   static constexpr int kTotal = kBarOffset + 1024 + 1024;  // barriers + alignment slack
 };
 
@@ -203,19 +204,24 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         row_base[i] = p.in_ptrs[n] + p.in_off;
       }
       if (aligned) {
-        // Filter-tap-major walk: row addresses once per (kh, kw), channel
-        // chunks are consecutive K tiles.
+        // Filter-tap-major walk: per (kh, kw) the 8 row sources and byte
+        // counts are computed once; each K tile is then 8 independent
+        // cp.async with hoisted smem offsets (no divisions, no selects).
         int tap = (w.kt0 * kBK) / p.Cin;
         int ci = w.kt0 * kBK - tap * p.Cin;
+        int kh = tap / p.KW, kw = tap - kh * p.KW;
+        uint32_t doff[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) doff[i] = swz(r0 + 16 * i, c);
         const float* src[8];
-        bool ok[8];
+        uint32_t nbytes[8];
         auto set_tap = [&] {
-          const int kh = tap / p.KW, kw = tap - (tap / p.KW) * p.KW;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int h = row_h[i] + kh, ww = row_w[i] + kw;
-            ok[i] = row_ok[i] && h >= 0 && h < p.H && ww >= 0 && ww < p.W;
-            src[i] = ok[i] ? row_base[i] + (static_cast<long>(h) * p.W + ww) * p.in_ldc + c * 4 : dummy;
+            const bool ok = row_ok[i] && h >= 0 && h < p.H && ww >= 0 && ww < p.W;
+            src[i] = ok ? row_base[i] + (h * p.W + ww) * p.in_ldc + c * 4 : dummy;
+            nbytes[i] = ok ? 16u : 0u;
           }
         };
         set_tap();
@@ -224,40 +230,54 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
           if (it >= STAGES) ptx::mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
           const uint32_t a_tile = smem_base + s * S::kStageBytes;
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            ptx::cp_async16(a_tile + swz(r0 + 16 * i, c), ok[i] ? src[i] + ci : dummy, ok[i] ? 16u : 0u);
+          for (int i = 0; i < 8; ++i) ptx::cp_async16(a_tile + doff[i], src[i] + ci, nbytes[i]);
           ptx::cp_async_arrive_noinc(&raw_full[s]);
           if (p.trace && t == 0 && it == 0) p.trace[8 + 4 * blockIdx.x + 2] = gtime();
+          if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
           ci += kBK;
           if (ci == p.Cin && kt + 1 < w.kt1) {
             ci = 0;
-            ++tap;
+            if (++kw == p.KW) {
+              kw = 0;
+              ++kh;
+            }
             set_tap();
           }
         }
       } else {
-        // Generic K decomposition (stem Cin = 4, narrow 1x1 inputs).
+        // Generic K walk (stem Cin = 4, narrow inputs): this thread's 4
+        // channels start at k = kt * 32 + 4c; the (ci, kw, kh) position is
+        // stepped by 32 per K tile without divisions.
+        uint32_t doff[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) doff[i] = swz(r0 + 16 * i, c);
+        int k0 = w.kt0 * kBK + c * 4;
+        int q = k0 / p.Cin;
+        int ci = k0 - q * p.Cin;
+        int kh = q / p.KW;
+        int kw = q - kh * p.KW;
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) ptx::mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
           const uint32_t a_tile = smem_base + s * S::kStageBytes;
-          const int k0 = kt * kBK + c * 4;
           const bool k_ok = k0 < p.K;
-          int ci = 0, kh = 0, kw = 0;
-          if (k_ok) {
-            const int q = k0 / p.Cin;
-            ci = k0 - q * p.Cin;
-            kh = q / p.KW;
-            kw = q - kh * p.KW;
-          }
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int h = row_h[i] + kh, ww = row_w[i] + kw;
             const bool ok = k_ok && row_ok[i] && h >= 0 && h < p.H && ww >= 0 && ww < p.W;
-            const float* srcp = ok ? row_base[i] + (static_cast<long>(h) * p.W + ww) * p.in_ldc + ci : dummy;
-            ptx::cp_async16(a_tile + swz(r0 + 16 * i, c), srcp, ok ? 16u : 0u);
+            const float* srcp = ok ? row_base[i] + (h * p.W + ww) * p.in_ldc + ci : dummy;
+            ptx::cp_async16(a_tile + doff[i], srcp, ok ? 16u : 0u);
           }
           ptx::cp_async_arrive_noinc(&raw_full[s]);
+          k0 += kBK;
+          ci += kBK;
+          while (ci >= p.Cin) {
+            ci -= p.Cin;
+            if (++kw == p.KW) {
+              kw = 0;
+              ++kh;
+            }
+          }
         }
       }
     }
@@ -285,6 +305,10 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
       const float* res_row =
           (m_ok && p.res_ptrs) ? p.res_ptrs[n_img] + p.res_off + static_cast<long>(pix) * p.res_ldc : nullptr;
       if (p.ksplits == 1) {
+        // Coalesced epilogue: each warp stages its 32 rows x 32 columns in
+        // shared memory (16B chunks XOR-swizzled by row), then writes whole
+        // 128-byte row segments (8 lanes per row, 4 rows per instruction).
+        const uint32_t stage = smem_base + S::kStagingOffset + ew * 32 * 128;
 #pragma unroll 1
         for (int jj = 0; jj < BN / 32; ++jj) {
           uint32_t v[32];
@@ -295,21 +319,55 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
             ptx::mbar_arrive(&acc_empty[acc]);  // TMEM buffer free for unit j + 2
           }
           const int n0 = w.n_base + jj * 32;
-          if (!m_ok || n0 >= p.N) continue;
-          const int ncols = min(32, p.N - n0);
-          float o[32];
+          if (n0 >= p.N) continue;  // warp-uniform
 #pragma unroll
-          for (int q = 0; q < 32; ++q) o[q] = q < ncols ? epilogue_op(p, __uint_as_float(v[q]), n0 + q, res_row) : 0.f;
-          float* dst = out_row + n0;
-          if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-#pragma unroll
-            for (int q = 0; q < 32; q += 4)
-              *reinterpret_cast<float4*>(dst + q) = make_float4(o[q], o[q + 1], o[q + 2], o[q + 3]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q < ncols) dst[q] = o[q];
+          for (int q = 0; q < 8; ++q)
+            ptx::sts128(stage + lane * 128 + ((q ^ (lane & 7)) << 4),
+                        make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                    __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+          __syncwarp();
+          const int cq = lane & 7;          // 16-byte chunk of the row segment
+          const int nc = n0 + cq * 4;       // first column of the chunk
+          const bool col_ok = nc < p.N;
+          const bool full4 = nc + 3 < p.N;
+          float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (p.bias && full4) b4 = make_float4(__ldg(p.bias + nc), __ldg(p.bias + nc + 1), __ldg(p.bias + nc + 2),
+                                                 __ldg(p.bias + nc + 3));
+#pragma unroll 4
+          for (int rq = 0; rq < 8; ++rq) {
+            const int rl = rq * 4 + (lane >> 3);  // row inside the warp's 32
+            const unsigned long long op =
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(out_row), rl);
+            const unsigned long long rp =
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(res_row), rl);
+            if (!op || !col_ok) continue;
+            float4 x = ptx::lds128(stage + rl * 128 + ((cq ^ (rl & 7)) << 4));
+            float* dst = reinterpret_cast<float*>(op) + nc;
+            const float* rr = reinterpret_cast<const float*>(rp);
+            const bool vec = full4 && ((reinterpret_cast<uintptr_t>(dst) | (rr ? reinterpret_cast<uintptr_t>(rr + nc) : 0)) & 15) == 0;
+            if (vec) {
+              x.x += b4.x; x.y += b4.y; x.z += b4.z; x.w += b4.w;
+              if (rr) {
+                const float4 r4 = *reinterpret_cast<const float4*>(rr + nc);
+                x.x += r4.x; x.y += r4.y; x.z += r4.z; x.w += r4.w;
+              }
+              if (p.relu == 1) {
+                x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+              } else if (p.relu == 2) {
+                x.x = fminf(fmaxf(x.x, 0.f), 6.f); x.y = fminf(fmaxf(x.y, 0.f), 6.f);
+                x.z = fminf(fmaxf(x.z, 0.f), 6.f); x.w = fminf(fmaxf(x.w, 0.f), 6.f);
+              }
+              if (p.round_out) {
+                x.x = ptx::round_tf32(x.x); x.y = ptx::round_tf32(x.y);
+                x.z = ptx::round_tf32(x.z); x.w = ptx::round_tf32(x.w);
+              }
+              *reinterpret_cast<float4*>(dst) = x;
+            } else {
+              const float xs[4] = {x.x, x.y, x.z, x.w};
+              for (int q = 0; q < 4 && nc + q < p.N; ++q) dst[q] = epilogue_op(p, xs[q], nc + q, rr);
+            }
           }
+          __syncwarp();
         }
       } else {
         // Split-K: park the raw partial tile; once all splits of the tile
@@ -395,6 +453,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         const int s = it % STAGES;
         ptx::mbar_wait(&mma_full[s], (it / STAGES) & 1);
         ptx::tc_fence_after();
+        if (p.trace && lane == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 4] = gtime();
         if (ptx::elect_one()) {
           const uint32_t a_tile = smem_base + s * S::kStageBytes;
           const uint32_t b_tile = a_tile + S::kABytes * (SPLIT ? 2 : 1);
@@ -427,6 +486,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
           const uint32_t b_tile = smem_base + s * S::kStageBytes + S::kABytes * (SPLIT ? 2 : 1);
           ptx::mbar_arrive_expect_tx(&raw_full[s], S::kBBytes);
           ptx::tma_load_2d(b_tile, &p.wmap, kt * kBK, w.n_base, &raw_full[s]);
+          if (p.trace && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 1] = gtime();
         }
       }
     }
@@ -437,25 +497,33 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
       const int t = threadIdx.x - 320;
       const int c = t & 7;
       const int r0 = t >> 3;
+      uint32_t doff[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) doff[i] = swz(r0 + 16 * i, c);
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit w = unit_of(p, u, BN, KT);
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % STAGES;
           ptx::mbar_wait(&raw_full[s], (it / STAGES) & 1);
+          if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 2] = gtime();
           const uint32_t a_hi = smem_base + s * S::kStageBytes;
           const uint32_t a_lo = a_hi + S::kABytes;
+          // All eight loads first (independent), then convert and store:
+          // keeps the chunk chains overlapped despite the volatile asm order.
+          float4 v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = ptx::lds128(a_hi + doff[i]);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const uint32_t o = swz(r0 + 16 * i, c);
-            const float4 v = ptx::lds128(a_hi + o);
-            const float4 h = make_float4(ptx::round_tf32(v.x), ptx::round_tf32(v.y), ptx::round_tf32(v.z),
-                                         ptx::round_tf32(v.w));
-            ptx::sts128(a_hi + o, h);
-            ptx::sts128(a_lo + o, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
+            const float4 h = make_float4(ptx::round_tf32(v[i].x), ptx::round_tf32(v[i].y),
+                                         ptx::round_tf32(v[i].z), ptx::round_tf32(v[i].w));
+            ptx::sts128(a_hi + doff[i], h);
+            ptx::sts128(a_lo + doff[i], make_float4(v[i].x - h.x, v[i].y - h.y, v[i].z - h.z, v[i].w - h.w));
           }
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&split_full[s]);
+          if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 3] = gtime();
         }
       }
     }

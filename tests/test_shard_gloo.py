@@ -1,0 +1,84 @@
+"""N > 1 path on CPU: request-stream sharding across ranks (gloo, world 2).
+
+Each rank routes the same global Poisson trace, serves its shard with the
+bit-exact scheduler (virtual time), and the ranks all-gather what they
+served: every request is served by exactly one rank, and each rank's trace is
+identical to the reference simulator on the same explicit sub-trace (when the
+oracle binary is available).
+"""
+import json
+import os
+import socket
+import subprocess
+import tempfile
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+REF = ROOT / "oracle" / "_ref" / "ref_dump"
+JOB = {"job": "sim", "profile": "tests/golden/ref_data/googlenet.json",
+       "workload": {"process": "poisson", "rate": 400, "count": 300, "seed": 11, "relative_deadline": 150},
+       "sim": {"scheduler": "ours-tardy", "granularity": "layer"}}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir, policy):
+    import torch
+    import torch.distributed as dist
+    os.chdir(ROOT)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    from paper_2304_09961_b200._native import host_call
+    from paper_2304_09961_b200.shard import shard_job
+    job, sh = shard_job(JOB, world, rank, policy)
+    # An empty shard serves nothing (explicit_arrivals = [] would mean "generate").
+    lines = host_call(job).splitlines() if sh.arrivals else []
+    outcomes = json.loads(lines[-2])["outcomes"] if lines else []
+    served = [sh.global_ids[o[0] - 1] for o in outcomes]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, served)
+    ok_ref = None
+    if REF.exists() and lines:
+        with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+            json.dump(job, f)
+        ref = subprocess.run([str(REF), f.name], capture_output=True, text=True, check=True).stdout.splitlines()
+        strip = lambda ls: [json.dumps({k: v for k, v in json.loads(l).items() if k != "wall_ms"}, sort_keys=True)
+                            for l in ls]
+        ok_ref = strip(ref) == strip(lines)
+    t = torch.tensor([len(served)], dtype=torch.int64)
+    dist.all_reduce(t)
+    if rank == 0:
+        Path(out_dir, "result.json").write_text(json.dumps({"gathered": gathered, "total": int(t.item())}))
+    Path(out_dir, f"ref{rank}.json").write_text(json.dumps(ok_ref))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", ["round_robin", "dnn_affine"])
+def test_sharded_serving_world2(tmp_path, policy):
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), policy), nprocs=world, join=True)
+    res = json.loads((tmp_path / "result.json").read_text())
+    flat = sorted(i for part in res["gathered"] for i in part)
+    assert res["total"] == 300
+    assert flat == list(range(1, 301))  # every request served exactly once
+    if policy == "round_robin":
+        assert all(len(p) == 150 for p in res["gathered"])
+    for r in range(world):
+        ok = json.loads((tmp_path / f"ref{r}.json").read_text())
+        assert ok in (None, True)  # None: oracle not built here
+
+
+def test_by_client_keeps_client_map():
+    from paper_2304_09961_b200.shard import route
+    arr = [(float(i), 0, 1000) for i in range(40)]
+    owners = route(arr, 4, "by_client", clients=8)
+    for gid, o in enumerate(owners, start=1):
+        assert o == ((gid - 1) % 8) % 4
