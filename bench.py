@@ -144,7 +144,11 @@ def run_ours(a, ws, rank, local) -> dict | None:
     layers = prof["components"][0]["layers"]
     t1 = sum(dict(L["runtime_ms"])[1] for L in layers)
     t90 = sum(dict(L["runtime_ms"])[90] for L in layers)
-    deadline = 6.25 * t1
+    # Fixed target: 5 ms = 6.25 x 0.8 ms, the best single-request GoogLeNet
+    # latency measured on this B200 build (SURVEY.md §8d sets D = 6.25 x T1,
+    # the paper's 150 ms / 24 ms ratio). It is a constant so that a kernel
+    # change cannot move the target; the current T1 is reported beside it.
+    deadline = a.deadline_ms
     base = {"profile": prof, "sim": {"scheduler": "ours-tardy", "granularity": "layer", "max_batch": 90},
             "image_pool": 64, "pipeline_depth": 2}
 
@@ -178,8 +182,10 @@ def run_ours(a, ws, rank, local) -> dict | None:
         if hi is not None and lo is not None and (hi - lo) / hi < 0.06 and len(warm_runs) >= a.warmup:
             break
         rate = 0.5 * (lo + hi) if (lo is not None and hi is not None) else rate
-    cap = lo if lo is not None else rate
-    cap = allreduce_max(-cap, ws) * -1.0  # same offered rate on every rank (the slowest rank's capacity)
+    cap_search = lo if lo is not None else rate
+    # Timed runs at 97% of the largest passing rate: the on-time ratio is steep
+    # near saturation and single runs vary by a few percent.
+    cap = allreduce_max(-cap_search, ws) * -0.97  # same offered rate on every rank
 
     # ---- timed steps at the capacity rate
     ex.stats(True, every=a.stats_every)
@@ -263,6 +269,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "workload": "config 2: GoogLeNet 224x224 single DNN, Poisson arrivals, Our-Tardy (on-time objective), "
                         "partial batching at layer granularity, B=90, 1 server per GPU",
             "offered_rate_per_gpu": round(cap, 1),
+            "capacity_search_rate": round(cap_search, 1),
             "requests_per_step": a.requests,
             "deadline_ms": round(deadline, 4),
             "t1_ms": round(t1, 4),
@@ -385,6 +392,7 @@ def main() -> None:
     ap.add_argument("--precision", default="tf32x2", choices=["tf32x2", "tf32"])
     ap.add_argument("--stats-every", type=int, default=4)
     ap.add_argument("--cpu-requests", type=int, default=4)
+    ap.add_argument("--deadline-ms", type=float, default=5.0)
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     ws, rank, local = dist_init()

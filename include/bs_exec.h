@@ -141,6 +141,10 @@ int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_host, const 
                    const float* bias_host, const float* res_host, float* out_host, int reps,
                    float* ms_per_launch);
 
+/* Max-pool (k <= 3) on host NHWC buffers; stride_pad = 16 * stride + pad. */
+int bs_kernel_maxpool(int nimg, int H, int W, int C, int Ho, int Wo, int k, int stride_pad, const float* in_host,
+                      float* out_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,12 +28,22 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   ck(cudaSetDevice(device), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
+  ck(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
   ck(cudaMalloc(&d_weights_, suite_.weights.size() * sizeof(float)), "weights");
   ck(cudaMemcpy(d_weights_, suite_.weights.data(), suite_.weights.size() * sizeof(float), cudaMemcpyHostToDevice),
      "weights H2D");
   for (const NetDef& n : suite_.nets) slot_floats_ = std::max<std::size_t>(slot_floats_, static_cast<std::size_t>(n.blob_floats));
   slot_floats_ = (slot_floats_ + 63) / 64 * 64;
   n_slots_ = max_requests;
+  ready_ring_.resize(static_cast<std::size_t>(n_slots_) + 256);
+  for (auto& e : ready_ring_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ready ring");
+  {
+    std::size_t mx = 0;
+    for (const NetDef& n : suite_.nets) mx = std::max<std::size_t>(mx, static_cast<std::size_t>(n.in_H) * n.in_W * 3);
+    staging_floats_ = (mx + 63) / 64 * 64;
+    staging_n_ = 64;
+    ck(cudaMalloc(&staging_, staging_floats_ * staging_n_ * sizeof(float)), "rgb staging");
+  }
   ck(cudaMalloc(&arena_, static_cast<std::size_t>(n_slots_) * slot_floats_ * sizeof(float)), "arena");
   for (int i = n_slots_ - 1; i >= 0; --i) free_.push_back(i);
   n_ride_ = std::max(2 * max_batch_, 16);
@@ -85,8 +95,9 @@ Executor::~Executor() {
     cudaFree(c.dev);
     cudaEventDestroy(c.done);
   }
-  for (auto& [id, s] : slot_of_)
-    if (s.ready) cudaEventDestroy(s.ready);
+  if (copy_) cudaStreamSynchronize(copy_);
+  for (cudaEvent_t e : ready_ring_) cudaEventDestroy(e);
+  cudaFree(staging_);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (float* p : pool_) cudaFree(p);
   cudaFree(conv_ws_.partials);
@@ -99,9 +110,19 @@ Executor::~Executor() {
   cudaFree(flush_);
   cudaStreamDestroy(stream_);
   cudaStreamDestroy(side_);
+  cudaStreamDestroy(copy_);
 }
 
-void Executor::sync() { ck(cudaStreamSynchronize(stream_), "sync"); }
+cudaEvent_t Executor::next_ready_event() {
+  cudaEvent_t e = ready_ring_[ready_next_];
+  ready_next_ = (ready_next_ + 1) % ready_ring_.size();
+  return e;
+}
+
+void Executor::sync() {
+  ck(cudaStreamSynchronize(copy_), "sync copy");
+  ck(cudaStreamSynchronize(stream_), "sync");
+}
 
 void Executor::set_precision(const std::string& mode) {
   if (mode == "tf32x2") split_ = true;
@@ -227,10 +248,14 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
   s.blob = slot_ptr(s.index);
   const TensorDef& in = net.tensors[static_cast<std::size_t>(net.input_t)];
   const std::size_t bytes = static_cast<std::size_t>(in.H) * in.W * in.C * sizeof(float);
-  cudaStream_t st = entry_layer > 1 ? side_ : stream_;
+  cudaStream_t st = entry_layer > 1 ? side_ : copy_;
   ck(cudaMemcpyAsync(s.blob + in.off, image, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
      "admit copy");
-  if (entry_layer > 1) {
+  if (entry_layer == 1) {
+    s.ready = next_ready_event();
+    ck(cudaEventRecord(s.ready, copy_), "ready rec");
+    s.pending_ready = true;
+  } else {
     // Collaborative mode: the client's layer prefix, emulated on a side
     // stream so it stays off the server's critical path.
     TableChunk& c = chunks_[chunk_];
@@ -253,10 +278,33 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
     std::swap(stream_, side_);
     ck(cudaEventRecord(mine.done, side_), "chunk done");
     mine.in_use = true;
-    ck(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming), "ready ev");
+    s.ready = next_ready_event();
     ck(cudaEventRecord(s.ready, side_), "ready rec");
     s.pending_ready = true;
   }
+  slot_of_.emplace(id, s);
+}
+
+void Executor::admit_rgb(std::int64_t id, int dnn, const float* rgb) {
+  if (slot_of_.count(id)) throw std::logic_error("request admitted twice: " + std::to_string(id));
+  if (free_.empty()) throw std::runtime_error("activation arena full");
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
+  const TensorDef& in = net.tensors[static_cast<std::size_t>(net.input_t)];
+  if (in.C != 4) throw std::invalid_argument("admit_rgb needs a 4-channel padded input");
+  Slot s;
+  s.index = free_.back();
+  free_.pop_back();
+  s.dnn = dnn;
+  s.blob = slot_ptr(s.index);
+  const int hw = in.H * in.W;
+  float* stage = staging_ + static_cast<std::size_t>(staging_next_) * staging_floats_;
+  staging_next_ = (staging_next_ + 1) % staging_n_;  // ring reuse is ordered on copy_
+  ck(cudaMemcpyAsync(stage, rgb, static_cast<std::size_t>(hw) * 3 * sizeof(float), cudaMemcpyHostToDevice, copy_),
+     "admit rgb H2D");
+  ck(launch_expand_rgb(stage, s.blob + in.off, hw, copy_), "expand rgb");
+  s.ready = next_ready_event();
+  ck(cudaEventRecord(s.ready, copy_), "ready rec");
+  s.pending_ready = true;
   slot_of_.emplace(id, s);
 }
 
@@ -293,10 +341,9 @@ void Executor::retire_async(std::int64_t id, float* out, int n) {
 void Executor::drop(std::int64_t id) {
   auto it = slot_of_.find(id);
   if (it == slot_of_.end()) return;
-  if (it->second.ready) {
-    // a pending prefix must finish before the slot can be reused
+  if (it->second.pending_ready) {
+    // a pending input copy / prefix must finish before the slot can be reused
     ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
-    cudaEventDestroy(it->second.ready);
   }
   free_.push_back(it->second.index);
   slot_of_.erase(it);
@@ -348,6 +395,10 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     if (r.join_layer > to || r.leave_layer < from) continue;
     auto it = slot_of_.find(r.id);
     if (it == slot_of_.end()) continue;  // dropped meanwhile
+    if (it->second.pending_ready) {
+      ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
+      it->second.pending_ready = false;
+    }
     auto rb = ride_of_.find(r.id);
     float* buf;
     if (rb == ride_of_.end()) {

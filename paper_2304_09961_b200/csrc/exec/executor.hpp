@@ -54,6 +54,10 @@ class Executor {
   // ---- request lifecycle
   // image: NHWC [in_H][in_W][in_C] floats, on host (copied H2D) or device.
   void admit(std::int64_t id, int dnn, int entry_layer, const float* image, bool on_device);
+  // Packed RGB [H][W][3] in pinned host memory: H2D on the copy stream into a
+  // staging ring, expanded to the padded input tensor on the device; the
+  // request's first step waits for it (copies overlap compute).
+  void admit_rgb(std::int64_t id, int dnn, const float* rgb_pinned);
   void retire(std::int64_t id, float* probs_host, int n, bool logits = false);  // synchronous copy
   void retire_async(std::int64_t id, float* probs_pinned, int n);               // stream-ordered copy + free
   void drop(std::int64_t id);
@@ -102,7 +106,7 @@ class Executor {
     int index = -1;
     int dnn = 0;
     float* blob = nullptr;
-    cudaEvent_t ready = nullptr;  // prefix (client-side layers) finished
+    cudaEvent_t ready = nullptr;  // input copy / client prefix finished (ring-owned)
     bool pending_ready = false;
   };
   float* slot_ptr(int index) const { return arena_ + static_cast<std::size_t>(index) * slot_floats_; }
@@ -114,6 +118,13 @@ class Executor {
   int max_batch_ = 90;
   cudaStream_t stream_ = nullptr;
   cudaStream_t side_ = nullptr;  // client-prefix emulation
+  cudaStream_t copy_ = nullptr;  // admissions (H2D / D2D input copies)
+  std::vector<cudaEvent_t> ready_ring_;
+  std::size_t ready_next_ = 0;
+  float* staging_ = nullptr;     // RGB staging ring
+  std::size_t staging_floats_ = 0;
+  int staging_n_ = 0, staging_next_ = 0;
+  cudaEvent_t next_ready_event();
   float* d_weights_ = nullptr;
   float* arena_ = nullptr;
   std::size_t slot_floats_ = 0;

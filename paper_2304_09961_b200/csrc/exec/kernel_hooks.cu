@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../kernels/conv_tc.cuh"
+#include "../kernels/simple_ops.cuh"
 #include "bs_exec.h"
 #include "errors.hpp"
 
@@ -121,5 +122,34 @@ done:
   if (e1) cudaEventDestroy(e1);
   cudaFree(ws.partials); cudaFree(ws.counters);
   cudaFree(din); cudaFree(dw); cudaFree(db); cudaFree(dout); cudaFree(dres); cudaFree(ptrs);
+  return rc;
+}
+
+// Max-pool on host buffers (stride_pad = 16 * stride + pad), for the kernel tests.
+extern "C" int bs_kernel_maxpool(int nimg, int H, int W, int C, int Ho, int Wo, int k, int stride_pad,
+                                 const float* in_host, float* out_host) {
+  using namespace bs200;
+  const std::size_t in_n = static_cast<std::size_t>(nimg) * H * W * C, out_n = static_cast<std::size_t>(nimg) * Ho * Wo * C;
+  float *din = nullptr, *dout = nullptr;
+  float** ptrs = nullptr;
+  int rc = BS_OK;
+  std::vector<float*> hp(2 * nimg);
+  cudaError_t e = cudaMalloc(&din, in_n * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, out_n * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&ptrs, 2 * nimg * sizeof(float*));
+  if (e == cudaSuccess) e = cudaMemcpy(din, in_host, in_n * 4, cudaMemcpyHostToDevice);
+  for (int i = 0; i < nimg; ++i) {
+    hp[i] = din + static_cast<std::size_t>(H) * W * C * i;
+    hp[nimg + i] = dout + static_cast<std::size_t>(Ho) * Wo * C * i;
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(ptrs, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    PoolParams p{nimg, H, W, C, Ho, Wo, k, stride_pad / 16, stride_pad % 16, ptrs, 0, C, ptrs + nimg, 0, C};
+    e = launch_maxpool(p, 0);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(out_host, dout, out_n * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) rc = bs_fail_cuda(e, "bs_kernel_maxpool");
+  cudaFree(din); cudaFree(dout); cudaFree(ptrs);
   return rc;
 }

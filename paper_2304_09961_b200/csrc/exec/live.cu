@@ -7,6 +7,7 @@
 #include <deque>
 #include <stdexcept>
 #include <thread>
+#include <vector>
 
 #include "bsb/jobs.hpp"
 #include "image.hpp"
@@ -63,15 +64,20 @@ json serve_live(Executor& ex, const json& j) {
   for (std::size_t d = 0; d < dnn_map.size(); ++d) {
     const int net = dnn_map[d];
     const NetDef& nd = suite.nets[static_cast<std::size_t>(net)];
-    img_floats[static_cast<std::size_t>(net)] = static_cast<std::size_t>(nd.in_H) * nd.in_W * nd.in_C;
+    // e2e runs ship packed RGB (3 channels) from pinned host memory.
+    img_floats[static_cast<std::size_t>(net)] = static_cast<std::size_t>(nd.in_H) * nd.in_W * 3;
     if (h2d) {
       if (!host_pool[static_cast<std::size_t>(net)]) {
         float* p = nullptr;
         if (cudaMallocHost(&p, img_floats[static_cast<std::size_t>(net)] * pool * sizeof(float)) != cudaSuccess)
           throw std::runtime_error("pinned image pool");
-        for (int i = 0; i < pool; ++i)
-          synth_image(image_seed, static_cast<std::uint64_t>(i), nd.in_H, nd.in_W, nd.in_C, 3,
-                      p + img_floats[static_cast<std::size_t>(net)] * static_cast<std::size_t>(i));
+        std::vector<float> padded(static_cast<std::size_t>(nd.in_H) * nd.in_W * nd.in_C);
+        for (int i = 0; i < pool; ++i) {
+          synth_image(image_seed, static_cast<std::uint64_t>(i), nd.in_H, nd.in_W, nd.in_C, 3, padded.data());
+          float* dst = p + img_floats[static_cast<std::size_t>(net)] * static_cast<std::size_t>(i);
+          for (long px = 0; px < static_cast<long>(nd.in_H) * nd.in_W; ++px)
+            for (int ch = 0; ch < 3; ++ch) dst[px * 3 + ch] = padded[static_cast<std::size_t>(px) * nd.in_C + ch];
+        }
         host_pool[static_cast<std::size_t>(net)] = p;
       }
     } else if (ex.pool_size(net) < pool) {
@@ -143,8 +149,7 @@ json serve_live(Executor& ex, const json& j) {
       const int net = dnn_map[static_cast<std::size_t>(b.dnn)];
       const int img = static_cast<int>(ai % static_cast<std::size_t>(pool));
       if (h2d) {
-        ex.admit(id, net, 1, host_pool[static_cast<std::size_t>(net)] + img_floats[static_cast<std::size_t>(net)] * img,
-                 false);
+        ex.admit_rgb(id, net, host_pool[static_cast<std::size_t>(net)] + img_floats[static_cast<std::size_t>(net)] * img);
         h2d_bytes += static_cast<long>(img_floats[static_cast<std::size_t>(net)] * sizeof(float));
       } else {
         ex.admit(id, net, 1, ex.pool_image(net, img), true);

@@ -16,32 +16,69 @@ int grid_for(long work) {
   return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
 }
 
+__device__ __forceinline__ float4 max4(float4 a, float4 b) {
+  return make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z), fmaxf(a.w, b.w));
+}
+
+// One thread per (image, output pixel, 4 channels); 32-bit index math
+// (every pooled tensor of a 90-request batch has < 2^31 float4s).
 __global__ void maxpool_kernel(const PoolParams p) {
   const int C4 = p.C >> 2;
-  const long total = static_cast<long>(p.nimg) * p.Ho * p.Wo * C4;
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int c4 = static_cast<int>(i % C4);
-    long r = i / C4;
-    const int wo = static_cast<int>(r % p.Wo);
+  const int total = p.nimg * p.Ho * p.Wo * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c4 = i % C4;
+    int r = i / C4;
+    const int wo = r % p.Wo;
     r /= p.Wo;
-    const int ho = static_cast<int>(r % p.Ho);
-    const int n = static_cast<int>(r / p.Ho);
+    const int ho = r % p.Ho;
+    const int n = r / p.Ho;
     const float* in = p.in_ptrs[n] + p.in_off + c4 * 4;
     const int h0 = ho * p.stride - p.pad, w0 = wo * p.stride - p.pad;
     const int hs = max(h0, 0), ws = max(w0, 0);
     const int he = min(h0 + p.k, p.H), we = min(w0 + p.k, p.W);
     float4 m = make_float4(-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX);
     for (int h = hs; h < he; ++h)
-      for (int w = ws; w < we; ++w) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(in + (static_cast<long>(h) * p.W + w) * p.in_ldc));
-        m.x = fmaxf(m.x, v.x);
-        m.y = fmaxf(m.y, v.y);
-        m.z = fmaxf(m.z, v.z);
-        m.w = fmaxf(m.w, v.w);
+      for (int w = ws; w < we; ++w) m = max4(m, __ldg(reinterpret_cast<const float4*>(in + (h * p.W + w) * p.in_ldc)));
+    *reinterpret_cast<float4*>(p.out_ptrs[n] + p.out_off + (ho * p.Wo + wo) * p.out_ldc + c4 * 4) = m;
+  }
+}
+
+// Row-sliding max-pool (k <= 3): a thread owns one output row of 4 channels
+// and walks it left to right; each input column's k-row maximum is computed
+// once and kept in a 3-entry ring, so a stride-1 3x3 pool loads every input
+// element once per output row (3 loads per output instead of 9) and the
+// index math is per row, not per output.
+__global__ void maxpool_rows_kernel(const PoolParams p) {
+  const int C4 = p.C >> 2;
+  const long total = static_cast<long>(p.nimg) * p.Ho * C4;
+  const float4 ninf = make_float4(-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX);
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int c4 = static_cast<int>(i % C4);
+    const long r = i / C4;
+    const int ho = static_cast<int>(r % p.Ho);
+    const int n = static_cast<int>(r / p.Ho);
+    const float* in = p.in_ptrs[n] + p.in_off + c4 * 4;
+    float* out = p.out_ptrs[n] + p.out_off + static_cast<long>(ho) * p.Wo * p.out_ldc + c4 * 4;
+    const int h0 = ho * p.stride - p.pad;
+    const int hs = max(h0, 0), he = min(h0 + p.k, p.H);
+    float4 ring[3] = {ninf, ninf, ninf};
+    int last = -1000000;
+    for (int wo = 0; wo < p.Wo; ++wo) {
+      const int w0 = wo * p.stride - p.pad;
+      const int need = w0 + p.k - 1;
+      for (int col = max(last + 1, w0); col <= need; ++col) {
+        float4 m = ninf;
+        if (col >= 0 && col < p.W)
+          for (int h = hs; h < he; ++h)
+            m = max4(m, __ldg(reinterpret_cast<const float4*>(in + (static_cast<long>(h) * p.W + col) * p.in_ldc)));
+        ring[((col % 3) + 3) % 3] = m;
       }
-    float* out = p.out_ptrs[n] + p.out_off + (static_cast<long>(ho) * p.Wo + wo) * p.out_ldc + c4 * 4;
-    *reinterpret_cast<float4*>(out) = m;
+      last = max(last, need);
+      float4 o = ring[((w0 % 3) + 3) % 3];
+      for (int kw = 1; kw < p.k; ++kw) o = max4(o, ring[(((w0 + kw) % 3) + 3) % 3]);
+      *reinterpret_cast<float4*>(out + static_cast<long>(wo) * p.out_ldc) = o;
+    }
   }
 }
 
@@ -141,11 +178,29 @@ __global__ void softmax_kernel(const SoftmaxParams p) {
   for (int j = lane; j < p.N; j += 32) y[j] = __expf(x[j] - m) * inv;
 }
 
+__global__ void expand_rgb_kernel(const float* __restrict__ rgb, float* __restrict__ dst, int hw) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += gridDim.x * blockDim.x) {
+    const float r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
+    reinterpret_cast<float4*>(dst)[i] = make_float4(r, g, b, 0.f);
+  }
+}
+
 }  // namespace
 
+cudaError_t launch_expand_rgb(const float* rgb, float* dst, int hw, cudaStream_t s) {
+  expand_rgb_kernel<<<grid_for(hw), kThreads, 0, s>>>(rgb, dst, hw);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {
-  if (p.C % 4) return cudaErrorInvalidValue;
-  maxpool_kernel<<<grid_for(static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4)), kThreads, 0, s>>>(p);
+  if (p.C % 4 || p.k > 3) return cudaErrorInvalidValue;
+  const long rows = static_cast<long>(p.nimg) * p.Ho * (p.C / 4);
+  // The row-sliding form loads each input once per row but serialises a
+  // row's outputs; it pays only when rows alone fill the GPU several times.
+  if (p.stride == 1 && rows >= 148L * 2048 * 2)
+    maxpool_rows_kernel<<<grid_for(rows), kThreads, 0, s>>>(p);
+  else
+    maxpool_kernel<<<grid_for(static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4)), kThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 

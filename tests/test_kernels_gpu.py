@@ -107,3 +107,25 @@ def test_conv_plain_tf32_on_fp32_inputs_is_worse():
     """Sanity: without the split, un-rounded inputs lose ~1e-3 (the MMA truncates)."""
     err = run_conv(2, 14, 14, 64, 128, 1, 1, 1, 0, raw_input=True)
     assert 1e-5 < err < 5e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,stride,pad,ceil,H", [(3, 1, 1, True, 14), (3, 2, 0, True, 112), (3, 2, 1, False, 56),
+                                                (2, 2, 0, True, 14), (3, 2, 0, True, 28), (3, 2, 0, True, 13)])
+def test_maxpool_in_executor_layers(k, stride, pad, ceil, H):
+    """Max-pool shapes of GoogLeNet/ResNet-50 through a one-op network
+    (the executor's own launch path) against the oracle."""
+    from oracle.layers import maxpool_nhwc
+    import ctypes as C
+    from paper_2304_09961_b200._native import exec_lib, fptr
+    lib = exec_lib()
+    lib.bs_kernel_maxpool.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(1)
+    n, c = 3, 64
+    x = rng.standard_normal((n, H, H, c)).astype(np.float32)
+    ref = maxpool_nhwc(x, k, stride, pad, ceil)
+    out = np.zeros_like(ref)
+    rc = lib.bs_kernel_maxpool(n, H, H, c, ref.shape[1], ref.shape[2], k, stride * 16 + pad, fptr(x), fptr(out))
+    assert rc == 0
+    assert np.array_equal(out, ref)
