@@ -1,5 +1,7 @@
 #include "executor.hpp"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -44,10 +46,13 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
     staging_n_ = 64;
     ck(cudaMalloc(&staging_, staging_floats_ * staging_n_ * sizeof(float)), "rgb staging");
   }
-  ck(cudaMalloc(&arena_, static_cast<std::size_t>(n_slots_) * slot_floats_ * sizeof(float)), "arena");
-  for (int i = n_slots_ - 1; i >= 0; --i) free_.push_back(i);
+  // One slot space: [request slots | ride buffers | profiler scratch], so a
+  // single TMA tensor map per layer input addresses every blob by slot index.
   n_ride_ = std::max(2 * max_batch_, 16);
-  ck(cudaMalloc(&ride_arena_, static_cast<std::size_t>(n_ride_) * slot_floats_ * sizeof(float)), "ride arena");
+  total_slots_ = static_cast<long>(n_slots_) + n_ride_ + max_batch_;
+  ck(cudaMalloc(&arena_, static_cast<std::size_t>(total_slots_) * slot_floats_ * sizeof(float)), "arena");
+  for (int i = n_slots_ - 1; i >= 0; --i) free_.push_back(i);
+  ride_arena_ = arena_ + static_cast<std::size_t>(n_slots_) * slot_floats_;
   for (int i = n_ride_ - 1; i >= 0; --i) ride_free_.push_back(i);
   int max_layers = 1;
   for (const NetDef& n : suite_.nets) max_layers = std::max(max_layers, n.num_layers());
@@ -59,7 +64,7 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
     ck(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming), "event");
   }
   // Scratch blobs for the profiler (max_batch of them) + an L2 flush buffer.
-  ck(cudaMalloc(&scratch_, static_cast<std::size_t>(max_batch_) * slot_floats_ * sizeof(float)), "scratch");
+  scratch_ = ride_arena_ + static_cast<std::size_t>(n_ride_) * slot_floats_;
   ck(cudaMemset(scratch_, 0, static_cast<std::size_t>(max_batch_) * slot_floats_ * sizeof(float)), "scratch zero");
   ck(cudaMalloc(&scratch_ptrs_, max_batch_ * sizeof(float*)), "scratch ptrs");
   std::vector<float*> hp(static_cast<std::size_t>(max_batch_));
@@ -67,11 +72,15 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   ck(cudaMemcpy(scratch_ptrs_, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice), "scratch ptrs H2D");
   pool_.assign(suite_.nets.size(), nullptr);
   pool_n_.assign(suite_.nets.size(), 0);
-  conv_ws_.partial_floats = conv_workspace_floats();
-  conv_ws_.n_counters = conv_workspace_counters();
-  ck(cudaMalloc(&conv_ws_.partials, conv_ws_.partial_floats * sizeof(float)), "split-K workspace");
-  ck(cudaMalloc(&conv_ws_.counters, conv_ws_.n_counters * sizeof(int)), "split-K counters");
-  ck(cudaMemset(conv_ws_.counters, 0, conv_ws_.n_counters * sizeof(int)), "split-K counters zero");
+  // Split-K workspaces: one per stream that launches convs (serving stream,
+  // client-prefix side stream), so concurrent launches never share counters.
+  for (ConvWorkspace* w : {&conv_ws_, &side_ws_}) {
+    w->partial_floats = conv_workspace_floats();
+    w->n_counters = conv_workspace_counters();
+    ck(cudaMalloc(&w->partials, w->partial_floats * sizeof(float)), "split-K workspace");
+    ck(cudaMalloc(&w->counters, w->n_counters * sizeof(int)), "split-K counters");
+    ck(cudaMemset(w->counters, 0, w->n_counters * sizeof(int)), "split-K counters zero");
+  }
   // One TMA descriptor per conv/FC weight matrix (weights never move).
   wmaps_.resize(suite_.nets.size());
   for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
@@ -82,6 +91,26 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
       if (op.kind != OpKind::conv) continue;
       if (!encode_weight_map(&wmaps_[n][i], d_weights_ + op.w_off, op.out.C, op.Kpad))
         throw std::runtime_error("cuTensorMapEncodeTiled failed for " + op.name);
+    }
+  }
+  // One activation tensor map per conv input (the slot space never moves).
+  // BS_CONV_TMA=1: feed conv activations by TMA boxes wherever the geometry
+  // allows (default: cp.async gather; see DESIGN.md §4 for the ingest limits).
+  const char* tma_env = std::getenv("BS_CONV_TMA");
+  const bool no_tma = !(tma_env && tma_env[0] == '1');
+  amaps_.resize(suite_.nets.size());
+  for (std::size_t n = 0; n < suite_.nets.size() && !no_tma; ++n) {
+    const NetDef& net = suite_.nets[n];
+    amaps_[n].resize(net.ops.size());
+    for (std::size_t i = 0; i < net.ops.size(); ++i) {
+      const OpDef& op = net.ops[i];
+      if (op.kind != OpKind::conv) continue;
+      const TensorDef& ti = net.tensors[static_cast<std::size_t>(op.in.t)];
+      ActMap& am = amaps_[n][i];
+      if (!conv_act_geometry(op.in.C, op.Ho, op.Wo, op.stride, &am.geom)) continue;
+      am.ok = encode_act_map(&am.map, arena_ + ti.off + op.in.coff, op.in.C, ti.W, ti.H, ti.C, total_slots_,
+                             static_cast<long>(slot_floats_), am.geom, op.stride);
+      if (!am.ok) throw std::runtime_error("activation tensor map failed for " + op.name);
     }
   }
 }
@@ -100,12 +129,12 @@ Executor::~Executor() {
   cudaFree(staging_);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (float* p : pool_) cudaFree(p);
-  cudaFree(conv_ws_.partials);
-  cudaFree(conv_ws_.counters);
+  for (ConvWorkspace* w : {&conv_ws_, &side_ws_}) {
+    cudaFree(w->partials);
+    cudaFree(w->counters);
+  }
   cudaFree(d_weights_);
   cudaFree(arena_);
-  cudaFree(ride_arena_);
-  cudaFree(scratch_);
   cudaFree(scratch_ptrs_);
   cudaFree(flush_);
   cudaStreamDestroy(stream_);
@@ -193,7 +222,14 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
       p.relu = op.relu;
       p.round_out = split_ ? 0 : op.round_out;
       p.split = split_ ? 1 : 0;
-      e = launch_conv_tc(p, conv_ws_, stream_);
+      {
+        const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
+        const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
+        if (ni < amaps_.size() && oi < amaps_[ni].size() && amaps_[ni][oi].ok)
+          conv_use_act_map(p, amaps_[ni][oi].map, amaps_[ni][oi].geom, arena_, static_cast<long>(slot_floats_),
+                           total_slots_);
+      }
+      e = launch_conv_tc(p, *ws_, stream_);
       break;
     }
     case OpKind::maxpool: {
@@ -269,13 +305,16 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
     host[0] = s.blob;
     ck(cudaMemcpyAsync(d, host, sizeof(float*), cudaMemcpyHostToDevice, side_), "table H2D");
     std::swap(stream_, side_);
+    ws_ = &side_ws_;
     try {
       for (int k = 1; k < entry_layer; ++k) run_layer(dnn, k, d, 1);
     } catch (...) {
       std::swap(stream_, side_);
+      ws_ = &conv_ws_;
       throw;
     }
     std::swap(stream_, side_);
+    ws_ = &conv_ws_;
     ck(cudaEventRecord(mine.done, side_), "chunk done");
     mine.in_use = true;
     s.ready = next_ready_event();

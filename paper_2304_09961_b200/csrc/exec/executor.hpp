@@ -157,7 +157,16 @@ class Executor {
   std::vector<float*> pool_;
   std::vector<int> pool_n_;
   std::vector<std::vector<CUtensorMap>> wmaps_;  // [net][op] weight tensor maps
-  ConvWorkspace conv_ws_;                         // split-K partials + tile counters
+  struct ActMap {
+    CUtensorMap map{};
+    ActGeom geom;
+    bool ok = false;
+  };
+  std::vector<std::vector<ActMap>> amaps_;        // [net][op] conv input maps over the slot space
+  long total_slots_ = 0;
+  ConvWorkspace conv_ws_;                         // split-K partials + tile counters (serving stream)
+  ConvWorkspace side_ws_;                         // the same for the client-prefix side stream
+  const ConvWorkspace* ws_ = &conv_ws_;           // workspace of the stream launching now
   bool split_ = true;
   bool stats_on_ = false;
   int stats_every_ = 1;

@@ -74,6 +74,20 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_off = d->out_coff;
     p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_off = d->res_coff;
     p.relu = d->relu; p.round_out = d->round_out; p.split = d->split;
+    {
+      // TMA activation path: the nimg input images are the slot space.
+      ActGeom g;
+      CUtensorMap amap;
+      const char* tma_env = std::getenv("BS_CONV_TMA");
+      if (tma_env && tma_env[0] == '1' && conv_act_geometry(d->Cin, d->Ho, d->Wo, d->stride, &g)) {
+        if (!encode_act_map(&amap, din + d->in_coff, d->Cin, d->W, d->H, d->in_ldc, nimg,
+                            static_cast<long>(in_img), g, d->stride)) {
+          rc = bs_fail(BS_ECUDA, "activation tensor map failed");
+          goto done;
+        }
+        conv_use_act_map(p, amap, g, din, static_cast<long>(in_img), nimg);
+      }
+    }
     unsigned long long* trace = nullptr;
     if (std::getenv("BS_CONV_TRACE")) {
       CK(cudaMalloc(&trace, 8 * 1400));

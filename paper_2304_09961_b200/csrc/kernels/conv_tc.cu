@@ -18,17 +18,17 @@ int sm_count() {
   return n;
 }
 
-template <int BN, int STAGES, bool SPLIT>
+template <int BN, bool SPLIT>
 cudaError_t launch_bn(const ConvParams& p, int grid, cudaStream_t stream) {
-  using S = conv_tc::Smem<BN, STAGES, SPLIT>;
+  using S = conv_tc::Cfg<BN, SPLIT>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc::conv_tc_kernel<BN, STAGES, SPLIT>,
+    cudaError_t e = cudaFuncSetAttribute(conv_tc::conv_tc_kernel<BN, SPLIT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  conv_tc::conv_tc_kernel<BN, STAGES, SPLIT><<<grid, S::kThreads, S::kTotal, stream>>>(p);
+  conv_tc::conv_tc_kernel<BN, SPLIT><<<grid, S::kThreads, S::kTotal, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -70,13 +70,66 @@ bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad) {
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool conv_act_geometry(int Cin, int Ho, int Wo, int stride, ActGeom* geom) {
+  if (Ho <= 0 || Wo <= 0 || Wo > 128 || stride < 1 || stride > 2) return false;
+  ActGeom g;
+  g.Wb = 1;
+  while (g.Wb < Wo) g.Wb *= 2;
+  int hp = 1;
+  while (hp < Ho) hp *= 2;
+  g.Hb = std::min(conv_tc::kBM / g.Wb, hp);
+  const int R = g.Wb * g.Hb;
+  if (R < 32 || conv_tc::kBM % R != 0) return false;
+  g.G = conv_tc::kBM / R;
+  g.tpi = (Ho + g.Hb - 1) / g.Hb;
+  if (g.G > 1 && g.tpi != 1) return false;
+  if (g.Wb * stride > 256 || g.Hb * stride > 256) return false;
+  g.g = Cin % 32 == 0 ? 32 : Cin % 16 == 0 ? 16 : Cin % 8 == 0 ? 8 : Cin % 4 == 0 ? 4 : 0;
+  if (!g.g) return false;
+  *geom = g;
+  return true;
+}
+
+bool encode_act_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
+                    long slot_floats, const ActGeom& g, int stride) {
+  const EncodeTiledFn encode = encode_fn();
+  if (!encode || (reinterpret_cast<uintptr_t>(base) & 15) || ldc % 4 || slot_floats % 4) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(slots)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ldc) * 4, static_cast<cuuint64_t>(W) * ldc * 4,
+                                 static_cast<cuuint64_t>(slot_floats) * 4};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(g.g), static_cast<cuuint32_t>(g.Wb * stride),
+                             static_cast<cuuint32_t>(g.Hb * stride), 1};
+  const cuuint32_t elem[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, elem,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, g.g == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& g, const float* slot_base,
+                      long slot_floats, long slots) {
+  p.amap = map;
+  p.a_tma = 1;
+  p.a_g = g.g;
+  p.Wb = g.Wb;
+  p.Hb = g.Hb;
+  p.G = g.G;
+  p.tpi = g.tpi;
+  p.slot_base = slot_base;
+  p.slot_floats = slot_floats;
+  p.oob_slot = static_cast<int>(slots);
+}
+
 cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t stream) {
   if (p.Cin % 4 != 0 || p.Kpad % conv_tc::kBK != 0 || p.Kpad < p.K || p.nimg <= 0)
     return cudaErrorInvalidValue;
   const int bn = conv_tile_n(p.N);
   const int sms = sm_count();
   const int KT = p.Kpad / conv_tc::kBK;
-  p.m_tiles = (p.nimg * p.Ho * p.Wo + conv_tc::kBM - 1) / conv_tc::kBM;
+  if (p.a_tma && (p.G < 1 || p.G > 4 || p.Wb * p.Hb * p.G != conv_tc::kBM || p.a_g % 4 || p.Cin % p.a_g))
+    return cudaErrorInvalidValue;
+  p.m_tiles = p.a_tma ? (p.G == 1 ? p.nimg * p.tpi : (p.nimg + p.G - 1) / p.G)
+                      : (p.nimg * p.Ho * p.Wo + conv_tc::kBM - 1) / conv_tc::kBM;
   p.n_tiles = (p.N + bn - 1) / bn;
   const int tiles = p.m_tiles * p.n_tiles;
   // Split K when the tiles cannot cover the SMs (small merged batches).
@@ -112,16 +165,16 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   const int grid = std::min(units, sms);
   static const bool log = std::getenv("BS_CONV_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d ws=%p\n", p.nimg * p.Ho * p.Wo, p.N,
-                 p.K, KT, bn, tiles, p.ksplits, grid, static_cast<void*>(ws.partials));
+    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d tma=%d box=%dx%dx%d g=%d\n",
+                 p.nimg * p.Ho * p.Wo, p.N, p.K, KT, bn, tiles, p.ksplits, grid, p.a_tma, p.Hb, p.Wb, p.G, p.a_g);
   if (p.split) {
-    if (bn == 32) return launch_bn<32, 4, true>(p, grid, stream);
-    if (bn == 64) return launch_bn<64, 4, true>(p, grid, stream);
-    return launch_bn<128, 4, true>(p, grid, stream);
+    if (bn == 32) return launch_bn<32, true>(p, grid, stream);
+    if (bn == 64) return launch_bn<64, true>(p, grid, stream);
+    return launch_bn<128, true>(p, grid, stream);
   }
-  if (bn == 32) return launch_bn<32, 6, false>(p, grid, stream);
-  if (bn == 64) return launch_bn<64, 6, false>(p, grid, stream);
-  return launch_bn<128, 6, false>(p, grid, stream);
+  if (bn == 32) return launch_bn<32, false>(p, grid, stream);
+  if (bn == 64) return launch_bn<64, false>(p, grid, stream);
+  return launch_bn<128, false>(p, grid, stream);
 }
 
 }  // namespace bs200

@@ -14,20 +14,27 @@
 // partial tiles go to a workspace and the CTA that finishes a tile last
 // reduces them in fixed split order (deterministic results).
 //
-// Loads (mixed TMA / cp.async):
-//   * B (weights, dense [N][Kpad]) by TMA, one 128B-swizzled 2D box per stage;
+// Loads and operands:
+//   * B (weights, dense [N][Kpad]) by TMA, one 128B-swizzled 2D box per stage,
+//     read by the tensor core from shared memory;
 //   * A gathered straight from the NHWC request blobs with cp.async (zero-fill
-//     = spatial padding and M/K tails). Every image of a merged batch has its
-//     own base pointer, so requests stay in their own arena slots: the batch
-//     is gathered by the loader and scattered by the epilogue with no copy
-//     kernels. Completion: cp.async.mbarrier.arrive.noinc.
+//     = spatial padding and M/K tails) into a raw shared-memory ring. Every
+//     image of a merged batch has its own base pointer, so requests stay in
+//     their own arena slots: the batch is gathered by the loader and
+//     scattered by the epilogue with no copy kernels.
+//     Completion: cp.async.mbarrier.arrive.noinc.
+//   * Converter warps move each landed raw A stage into TMEM (tcgen05.st) as
+//     the MMA's A operand (tcgen05.mma ... [a_tmem] form) and free the raw
+//     stage at once, so the gather runs RA stages ahead of the converters
+//     instead of waiting for the MMAs of the stage it overwrites.
 //   * 2xTF32 split-A (default precision): weights are exactly TF32, so
 //     A*W = A_hi*W + A_lo*W with A_hi = rn_tf32(A) recovers ~fp32 accuracy at
-//     two MMAs per K step and no extra HBM traffic; splitter warps rewrite
-//     each landed A stage into [A_hi | A_lo].
+//     two MMAs per K step and no extra HBM or shared-memory traffic (A_lo
+//     lives in TMEM next to A_hi).
 //
-// Warp roles: 0-3 A producers, 4-7 epilogue (TMEM lanes 0-127), 8 MMA issuer
-// (+ TMEM owner), 9 B TMA issuer, 10-13 splitters (2xTF32 only).
+// Warp roles: 0-3 A cp.async producers (or, with TMA activations, a second
+// converter group), 4-7 epilogue (TMEM lanes 0-127), 8 MMA issuer (+ TMEM
+// owner), 9 B TMA issuer, 10-13 A converters, 14 A TMA issuer.
 #pragma once
 #include <cstdint>
 
@@ -65,6 +72,17 @@ struct ConvParams {
   float* partials;              // [units][128][BN] split-K workspace
   int* counters;                // [tiles] zero between launches (reset by the reducer)
   unsigned long long* trace;    // debug timeline of CTA 0 (nullptr in production)
+  // TMA activation path (a_tma = 1): A tiles are (Hb x Wb) output-pixel boxes
+  // of one image each, loaded per filter tap by a 4D tensor map over the whole
+  // slot space {C, W, H, slot} (zero fill = padding, element strides = conv
+  // stride). G = 128 / (Hb * Wb) images per 128-row M tile.
+  CUtensorMap amap;
+  int a_tma;
+  int a_g;                      // channels per box (32, 16, 8 or 4)
+  int Wb, Hb, G, tpi;           // box geometry; tpi = M tiles per image (G == 1)
+  const float* slot_base;       // slot index of an image = (in_ptrs[i] - slot_base) / slot_floats
+  long slot_floats;
+  int oob_slot;                 // a slot coordinate past the map (zero-filled boxes)
 };
 
 // Device workspace for split-K (owned by the caller; counters zeroed once).
@@ -78,17 +96,32 @@ struct ConvWorkspace {
 namespace conv_tc {
 
 constexpr int kBM = 128;
-constexpr int kBK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int kBK = 32;  // fp32 elements per 128-byte K row
 
-template <int BN, int STAGES, bool SPLIT>
-struct Smem {
-  static constexpr int kThreads = SPLIT ? 448 : 320;
+// Pipeline geometry per N tile. Three rings decouple the stages so no load
+// waits on an MMA it does not feed:
+//   raw A  (smem, RA x 16 KB): cp.async gather target; freed as soon as the
+//          converter warps have read a stage (not when the MMA finishes);
+//   B      (smem, NB x BN*128 B): weights by TMA, 128B-swizzled for UMMA;
+//   A op   (TMEM, TA slots): converted A operand, [hi | lo] for 2xTF32;
+//          the MMAs read A from TMEM, so shared memory only serves B to the
+//          tensor core.
+template <int BN, bool SPLIT>
+struct Cfg {
+  static constexpr int kThreads = 480;
+  static constexpr int RA = BN == 32 ? 10 : 8;
+  static constexpr int NB = BN == 128 ? 5 : 8;
+  static constexpr int kACols = SPLIT ? 2 * kBK : kBK;          // TMEM columns per A slot
+  static constexpr int kTA0 = 2 * BN;                            // first A column (after 2 accumulators)
+  static constexpr int TA = (512 - kTA0) / kACols < 8 ? (512 - kTA0) / kACols : 8;
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
-  static constexpr int kStageBytes = kABytes * (SPLIT ? 2 : 1) + kBBytes;  // [A_hi | A_lo | B]
-  static constexpr int kStagingOffset = STAGES * kStageBytes;  // epilogue staging, 128 x 32 fp32
+  static constexpr int kBOffset = RA * kABytes;
+  static constexpr int kStagingOffset = kBOffset + NB * kBBytes;  // epilogue staging, 128 x 32 fp32
   static constexpr int kBarOffset = kStagingOffset + kBM * 32 * 4;
-  static constexpr int kTotal = kBarOffset + 1024 + 1024;  // barriers + alignment slack
+  static constexpr int kTotal = kBarOffset + 512 + 1024;        // barriers + alignment slack
+  static_assert(kTotal <= 232448, "shared memory budget");
+  static_assert(TA >= 2, "TMEM budget");
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -106,7 +139,7 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 }
 
 struct Unit {
-  int m_base, n_base, tile, split, kt0, kt1;
+  int mt, m_base, n_base, tile, split, kt0, kt1;
 };
 
 __device__ __forceinline__ Unit unit_of(const ConvParams& p, int u, int BN, int KT) {
@@ -115,11 +148,37 @@ __device__ __forceinline__ Unit unit_of(const ConvParams& p, int u, int BN, int 
   w.tile = u / p.ksplits;
   const int mt = w.tile % p.m_tiles;  // consecutive tiles share a weight slice
   const int nt = w.tile / p.m_tiles;
+  w.mt = mt;
   w.m_base = mt * kBM;
   w.n_base = nt * BN;
   w.kt0 = w.split * p.kt_per_split;
   w.kt1 = min(KT, w.kt0 + p.kt_per_split);
   return w;
+}
+
+// Output pixel of row r of M tile mt: image and pixel index, false for
+// padding rows (M tail; box columns/rows outside the output in TMA mode).
+__device__ __forceinline__ bool row_pixel(const ConvParams& p, int mt, int r, int& img, int& pix) {
+  if (!p.a_tma) {
+    const int m = mt * kBM + r;
+    const int HoWo = p.Ho * p.Wo;
+    img = m / HoWo;
+    pix = m - img * HoWo;
+    return m < p.nimg * HoWo;
+  }
+  const int R = kBM / p.G;
+  const int b = r / R, rr = r - b * R;
+  const int dh = rr / p.Wb, dw = rr - dh * p.Wb;
+  int h;
+  if (p.G == 1) {
+    img = mt / p.tpi;
+    h = (mt - img * p.tpi) * p.Hb + dh;
+  } else {
+    img = mt * p.G + b;
+    h = dh;
+  }
+  pix = h * p.Wo + dw;
+  return img < p.nimg && h < p.Ho && dw < p.Wo;
 }
 
 __device__ __forceinline__ float epilogue_op(const ConvParams& p, float x, int n, const float* res_row) {
@@ -131,21 +190,23 @@ __device__ __forceinline__ float epilogue_op(const ConvParams& p, float x, int n
   return x;
 }
 
-template <int BN, int STAGES, bool SPLIT>
-__global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
+template <int BN, bool SPLIT>
+__global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p) {
-  using S = Smem<BN, STAGES, SPLIT>;
+  using S = Cfg<BN, SPLIT>;
+  constexpr int RA = S::RA, NB = S::NB, TA = S::TA;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
-  uint64_t* split_full = raw_full + STAGES;
-  uint64_t* empty_bar = split_full + STAGES;
-  uint64_t* acc_full = empty_bar + STAGES;  // [2]
-  uint64_t* acc_empty = acc_full + 2;       // [2]
+  uint64_t* ra_full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* ra_empty = ra_full + RA;
+  uint64_t* b_full = ra_empty + RA;
+  uint64_t* b_empty = b_full + NB;
+  uint64_t* ta_full = b_empty + NB;
+  uint64_t* ta_empty = ta_full + TA;
+  uint64_t* acc_full = ta_empty + TA;  // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  int* red_flag = reinterpret_cast<int*>(tmem_slot + 1);
-  uint64_t* mma_full = SPLIT ? split_full : raw_full;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -157,10 +218,18 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
   if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x] = gtime();
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&raw_full[s], 128 + 1);  // 128 cp.async arrivals + the TMA expect_tx
-      ptx::mbar_init(&split_full[s], 128);
-      ptx::mbar_init(&empty_bar[s], 1);
+    for (int s = 0; s < RA; ++s) {
+      // TMA: one arrive.expect_tx; cp.async: one .noinc arrival per producer thread
+      ptx::mbar_init(&ra_full[s], p.a_tma ? 1 : 128);
+      ptx::mbar_init(&ra_empty[s], 128);
+    }
+    for (int s = 0; s < NB; ++s) {
+      ptx::mbar_init(&b_full[s], 1);
+      ptx::mbar_init(&b_empty[s], 1);
+    }
+    for (int s = 0; s < TA; ++s) {
+      ptx::mbar_init(&ta_full[s], 128);
+      ptx::mbar_init(&ta_empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
@@ -169,14 +238,129 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
     ptx::fence_mbar_init();
   }
   if (warp == 9 && lane == 0) ptx::prefetch_tmap(&p.wmap);
-  if (warp == 8) ptx::tmem_alloc<2 * BN>(tmem_slot);
+  if (warp == 0 && lane == 0 && p.a_tma) ptx::prefetch_tmap(&p.amap);
+  if (warp == 8) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x + 1] = gtime();
 
-  if (warp < 4) {
+  // Converter: thread = one A row (TMEM lane). Reads its 128-byte row of a
+  // landed raw stage, frees the stage, and writes the MMA operand into its
+  // TMEM lane: rn_tf32(a) (+ the residual a - rn_tf32(a) for 2xTF32). With
+  // TMA activations two converter groups (warps 10-13 and 0-3) take
+  // alternate K tiles so the conversion latency overlaps.
+  auto convert = [&](int group, int ngroups, int trace_tid) {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    uint32_t roff[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) roff[c] = swz(row, c);
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + S::kTA0;
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = unit_of(p, u, BN, KT);
+      for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+        if (it % ngroups != group) continue;
+        const int s = it % RA;
+        ptx::mbar_wait(&ra_full[s], (it / RA) & 1);
+        if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 2] = gtime();
+        const uint32_t a_raw = smem_base + s * S::kABytes;
+        float4 v[8];
+        if (!p.a_tma || p.a_g == kBK) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = ptx::lds128(a_raw + roff[c]);
+        } else {
+          // TMA pieces of g channels: piece j = [128 rows][g] floats.
+          const int cpp = p.a_g / 4;  // 16-byte chunks per row of a piece
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int j = c / cpp, cc = c - j * cpp;
+            v[c] = ptx::lds128(a_raw + j * (kBM * p.a_g * 4) + row * (p.a_g * 4) + cc * 16);
+          }
+        }
+        ptx::mbar_arrive(&ra_empty[s]);
+        uint32_t hi[32];
+        [[maybe_unused]] uint32_t lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float x[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float h = ptx::round_tf32(x[e]);
+            hi[4 * c + e] = __float_as_uint(h);
+            if constexpr (SPLIT) lo[4 * c + e] = __float_as_uint(x[e] - h);
+          }
+        }
+        const int sa = it % TA;
+        if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t dst = lane_base + sa * S::kACols;
+        ptx::tmem_st32(dst, hi);
+        if constexpr (SPLIT) ptx::tmem_st32(dst + kBK, lo);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&ta_full[sa]);
+        if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 3] = gtime();
+      }
+    }
+  };
+
+  if (warp < 4 && p.a_tma) {
+    convert(1, 2, 0);
+  } else if (warp == 14) {
+    // ------------------------------------------------------ A by TMA boxes
+    // K tile kt = 32 / g boxes per image of the tile: k = kt * 32 + j * g
+    // -> (tap, ci); box origin = (ci, w0 * s - pad + kw, h0 * s - pad + kh,
+    // slot). Boxes past K or past the batch are aimed outside the map so the
+    // stage is zero-filled and the byte count stays constant.
+    if (p.a_tma && lane == 0) {
+      const int R = kBM / p.G;
+      const int pieces = kBK / p.a_g;
+      const uint32_t box_bytes = static_cast<uint32_t>(R * p.a_g * 4);
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = unit_of(p, u, BN, KT);
+        int slot[4], h0[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          int img;
+          if (p.G == 1) {
+            img = w.mt / p.tpi;
+            h0[b] = (w.mt - img * p.tpi) * p.Hb;
+          } else {
+            img = w.mt * p.G + b;
+            h0[b] = 0;
+          }
+          slot[b] = (b < p.G && img < p.nimg)
+                        ? static_cast<int>((p.in_ptrs[img] - p.slot_base) / p.slot_floats)
+                        : p.oob_slot;
+        }
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+          const int s = it % RA;
+          if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&ra_full[s], S::kABytes);
+          const uint32_t a_tile = smem_base + s * S::kABytes;
+          for (int j = 0; j < pieces; ++j) {
+            const int k = kt * kBK + j * p.a_g;
+            int tap = k / p.Cin;
+            int ci = k - tap * p.Cin;
+            if (k >= p.K) {
+              tap = 0;
+              ci = p.Cin;  // past dim 0: zeros
+            }
+            const int kh = tap / p.KW, kw = tap - kh * p.KW;
+            for (int b = 0; b < p.G; ++b)
+              ptx::tma_load_4d(a_tile + j * (kBM * p.a_g * 4) + b * box_bytes, &p.amap, ci, kw - p.pad,
+                               h0[b] * p.stride - p.pad + kh, slot[b], &ra_full[s]);
+          }
+          if (p.trace && it == 0) p.trace[8 + 4 * blockIdx.x + 2] = gtime();
+          if (p.trace && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
+        }
+      }
+    }
+  } else if (warp < 4) {
     // ------------------------------------------------------------ A gather
     const int t = threadIdx.x;
     const int c = t & 7;    // 16-byte chunk inside the 128-byte K row
@@ -203,6 +387,9 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         row_w[i] = wo * p.stride - p.pad;
         row_base[i] = p.in_ptrs[n] + p.in_off;
       }
+      uint32_t doff[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) doff[i] = swz(r0 + 16 * i, c);
       if (aligned) {
         // Filter-tap-major walk: per (kh, kw) the 8 row sources and byte
         // counts are computed once; each K tile is then 8 independent
@@ -210,9 +397,6 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         int tap = (w.kt0 * kBK) / p.Cin;
         int ci = w.kt0 * kBK - tap * p.Cin;
         int kh = tap / p.KW, kw = tap - kh * p.KW;
-        uint32_t doff[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) doff[i] = swz(r0 + 16 * i, c);
         const float* src[8];
         uint32_t nbytes[8];
         auto set_tap = [&] {
@@ -226,12 +410,12 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         };
         set_tap();
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-          const int s = it % STAGES;
-          if (it >= STAGES) ptx::mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
-          const uint32_t a_tile = smem_base + s * S::kStageBytes;
+          const int s = it % RA;
+          if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
+          const uint32_t a_tile = smem_base + s * S::kABytes;
 #pragma unroll
           for (int i = 0; i < 8; ++i) ptx::cp_async16(a_tile + doff[i], src[i] + ci, nbytes[i]);
-          ptx::cp_async_arrive_noinc(&raw_full[s]);
+          ptx::cp_async_arrive_noinc(&ra_full[s]);
           if (p.trace && t == 0 && it == 0) p.trace[8 + 4 * blockIdx.x + 2] = gtime();
           if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
           ci += kBK;
@@ -248,18 +432,15 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         // Generic K walk (stem Cin = 4, narrow inputs): this thread's 4
         // channels start at k = kt * 32 + 4c; the (ci, kw, kh) position is
         // stepped by 32 per K tile without divisions.
-        uint32_t doff[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) doff[i] = swz(r0 + 16 * i, c);
         int k0 = w.kt0 * kBK + c * 4;
         int q = k0 / p.Cin;
         int ci = k0 - q * p.Cin;
         int kh = q / p.KW;
         int kw = q - kh * p.KW;
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-          const int s = it % STAGES;
-          if (it >= STAGES) ptx::mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
-          const uint32_t a_tile = smem_base + s * S::kStageBytes;
+          const int s = it % RA;
+          if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
+          const uint32_t a_tile = smem_base + s * S::kABytes;
           const bool k_ok = k0 < p.K;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -268,7 +449,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
             const float* srcp = ok ? row_base[i] + (h * p.W + ww) * p.in_ldc + ci : dummy;
             ptx::cp_async16(a_tile + doff[i], srcp, ok ? 16u : 0u);
           }
-          ptx::cp_async_arrive_noinc(&raw_full[s]);
+          ptx::cp_async_arrive_noinc(&ra_full[s]);
           k0 += kBK;
           ci += kBK;
           while (ci >= p.Cin) {
@@ -293,14 +474,8 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
       ptx::mbar_wait(&acc_full[acc], (j >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-      const int m = w.m_base + row;
-      const bool m_ok = m < M;
       int n_img = 0, pix = 0;
-      if (m_ok) {
-        const int HoWo = p.Ho * p.Wo;
-        n_img = m / HoWo;
-        pix = m - n_img * HoWo;
-      }
+      const bool m_ok = row_pixel(p, w.mt, row, n_img, pix);
       float* out_row = m_ok ? p.out_ptrs[n_img] + p.out_off + static_cast<long>(pix) * p.out_ldc : nullptr;
       const float* res_row =
           (m_ok && p.res_ptrs) ? p.res_ptrs[n_img] + p.res_off + static_cast<long>(pix) * p.res_ldc : nullptr;
@@ -407,9 +582,9 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
         for (int idx = et; idx < (r_hi - r_lo) * kVec; idx += 128) {
           const int rr = r_lo + idx / kVec;
           const int c4 = idx - (idx / kVec) * kVec;
-          const int mm = w.m_base + rr;
           const int n0 = w.n_base + c4 * 4;
-          if (mm >= M || n0 >= p.N) continue;
+          int img, px;
+          if (!row_pixel(p, w.mt, rr, img, px) || n0 >= p.N) continue;
           float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
           for (int sp = 0; sp < p.ksplits; ++sp) {
             const float4 x = __ldcg(reinterpret_cast<const float4*>(
@@ -419,8 +594,6 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
             acc4.z += x.z;
             acc4.w += x.w;
           }
-          const int HoWo = p.Ho * p.Wo;
-          const int img = mm / HoWo, px = mm - (mm / HoWo) * HoWo;
           float* orow = p.out_ptrs[img] + p.out_off + static_cast<long>(px) * p.out_ldc;
           const float* rrow = p.res_ptrs ? p.res_ptrs[img] + p.res_off + static_cast<long>(px) * p.res_ldc : nullptr;
           const float vals[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
@@ -442,6 +615,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
   } else if (warp == 8) {
     // ---------------------------------------------------------- MMA issue
     constexpr uint32_t idesc = ptx::make_idesc(2, kBM, BN);
+    const uint32_t a_tmem0 = tmem_base + S::kTA0;
     int it = 0, j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = unit_of(p, u, BN, KT);
@@ -450,25 +624,22 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-        const int s = it % STAGES;
-        ptx::mbar_wait(&mma_full[s], (it / STAGES) & 1);
+        const int sa = it % TA, sb = it % NB;
+        ptx::mbar_wait(&ta_full[sa], (it / TA) & 1);
+        ptx::mbar_wait(&b_full[sb], (it / NB) & 1);
         ptx::tc_fence_after();
         if (p.trace && lane == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 4] = gtime();
         if (ptx::elect_one()) {
-          const uint32_t a_tile = smem_base + s * S::kStageBytes;
-          const uint32_t b_tile = a_tile + S::kABytes * (SPLIT ? 2 : 1);
-          const uint64_t a_desc = ptx::sw128_kmajor_desc(a_tile);
-          const uint64_t b_desc = ptx::sw128_kmajor_desc(b_tile);
+          const uint32_t a_slot = a_tmem0 + sa * S::kACols;
+          const uint64_t b_desc = ptx::sw128_kmajor_desc(smem_base + S::kBOffset + sb * S::kBBytes);
 #pragma unroll
           for (int k = 0; k < kBK / 8; ++k) {
-            // +32 bytes per K=8 step inside the swizzled row (>>4 -> +2).
-            ptx::mma_tf32(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
-            if constexpr (SPLIT) {
-              const uint64_t lo_desc = ptx::sw128_kmajor_desc(a_tile + S::kABytes);
-              ptx::mma_tf32(d_tmem, lo_desc + 2 * k, b_desc + 2 * k, idesc, 1);
-            }
+            // A: 8 TMEM columns per K=8 step; B: +32 bytes inside the swizzled row.
+            ptx::mma_tf32_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
+            if constexpr (SPLIT) ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
           }
-          ptx::mma_commit(&empty_bar[s]);
+          ptx::mma_commit(&ta_empty[sa]);
+          ptx::mma_commit(&b_empty[sb]);
           if (kt == w.kt1 - 1) ptx::mma_commit(&acc_full[acc]);
         }
         __syncwarp();
@@ -481,52 +652,17 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit w = unit_of(p, u, BN, KT);
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-          const int s = it % STAGES;
-          if (it >= STAGES) ptx::mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
-          const uint32_t b_tile = smem_base + s * S::kStageBytes + S::kABytes * (SPLIT ? 2 : 1);
-          ptx::mbar_arrive_expect_tx(&raw_full[s], S::kBBytes);
-          ptx::tma_load_2d(b_tile, &p.wmap, kt * kBK, w.n_base, &raw_full[s]);
+          const int s = it % NB;
+          if (it >= NB) ptx::mbar_wait(&b_empty[s], ((it / NB) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&b_full[s], S::kBBytes);
+          ptx::tma_load_2d(smem_base + S::kBOffset + s * S::kBBytes, &p.wmap, kt * kBK, w.n_base, &b_full[s]);
           if (p.trace && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 1] = gtime();
         }
       }
     }
     __syncwarp();
-  } else {
-    // --------------------------------------------------- 2xTF32 splitters
-    if constexpr (SPLIT) {
-      const int t = threadIdx.x - 320;
-      const int c = t & 7;
-      const int r0 = t >> 3;
-      uint32_t doff[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) doff[i] = swz(r0 + 16 * i, c);
-      int it = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit w = unit_of(p, u, BN, KT);
-        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-          const int s = it % STAGES;
-          ptx::mbar_wait(&raw_full[s], (it / STAGES) & 1);
-          if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 2] = gtime();
-          const uint32_t a_hi = smem_base + s * S::kStageBytes;
-          const uint32_t a_lo = a_hi + S::kABytes;
-          // All eight loads first (independent), then convert and store:
-          // keeps the chunk chains overlapped despite the volatile asm order.
-          float4 v[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = ptx::lds128(a_hi + doff[i]);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 h = make_float4(ptx::round_tf32(v[i].x), ptx::round_tf32(v[i].y),
-                                         ptx::round_tf32(v[i].z), ptx::round_tf32(v[i].w));
-            ptx::sts128(a_hi + doff[i], h);
-            ptx::sts128(a_lo + doff[i], make_float4(v[i].x - h.x, v[i].y - h.y, v[i].z - h.z, v[i].w - h.w));
-          }
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&split_full[s]);
-          if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 3] = gtime();
-        }
-      }
-    }
+  } else if (warp >= 10 && warp < 14) {
+    convert(0, p.a_tma ? 2 : 1, 320);
   }
 
   ptx::tc_fence_before();
@@ -534,7 +670,7 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
   if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x + 3] = gtime();
   if (warp == 8) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<2 * BN>(tmem_base);
+    ptx::tmem_dealloc<512>(tmem_base);
   }
 }
 
@@ -542,6 +678,25 @@ __global__ void __launch_bounds__(Smem<BN, STAGES, SPLIT>::kThreads, 1)
 
 // N tile the launcher uses for N output channels.
 int conv_tile_n(int N);
+
+// Box geometry of the TMA activation path for a conv with Cin (padded)
+// input channels and an Ho x Wo output: Wb = next power of two >= Wo,
+// Hb = min(128 / Wb, next power of two >= Ho), G = 128 / (Wb * Hb) images per
+// M tile, g = channels per box. False when the layer does not fit the path
+// (tiny outputs such as FC layers, G > 4): it then uses the cp.async gather.
+struct ActGeom {
+  int Wb = 0, Hb = 0, G = 0, tpi = 0, g = 0;
+};
+bool conv_act_geometry(int Cin, int Ho, int Wo, int stride, ActGeom* geom);
+// Tensor map over a slot space of `slots` request blobs of `slot_floats`
+// floats each: {C, W, H, slot} starting at `base` (the tensor's first channel
+// in slot 0), box {g, Wb * stride, Hb * stride, 1}, element strides
+// {1, stride, stride, 1}; 128B swizzle when g == 32.
+bool encode_act_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
+                    long slot_floats, const ActGeom& geom, int stride);
+// Fills the TMA fields of p (a_tma = 1) from a geometry and an encoded map.
+void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& geom, const float* slot_base,
+                      long slot_floats, long slots);
 // Encodes a weight tensor map for w ([N][Kpad] floats) and the tile conv_tile_n(N).
 bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad);
 // Host-side launcher: chooses the K split, grid and workspace use

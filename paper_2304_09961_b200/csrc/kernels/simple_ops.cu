@@ -43,6 +43,40 @@ __global__ void maxpool_kernel(const PoolParams p) {
   }
 }
 
+// k x k max-pool, fully unrolled: one thread per (image, output pixel, 4
+// channels), consecutive threads on consecutive channel quads (coalesced
+// 16-byte loads/stores); all k*k window loads are independent and predicated
+// so they are in flight together.
+template <int K>
+__global__ void __launch_bounds__(256) maxpool_unrolled_kernel(const PoolParams p) {
+  const int C4 = p.C >> 2;
+  const int total = p.nimg * p.Ho * p.Wo * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c4 = i % C4;
+    int r = i / C4;
+    const int wo = r % p.Wo;
+    r /= p.Wo;
+    const int ho = r % p.Ho;
+    const int n = r / p.Ho;
+    const float* in = p.in_ptrs[n] + p.in_off + c4 * 4;
+    const int h0 = ho * p.stride - p.pad, w0 = wo * p.stride - p.pad;
+    float4 v[K * K];
+#pragma unroll
+    for (int kh = 0; kh < K; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < K; ++kw) {
+        const int h = h0 + kh, w = w0 + kw;
+        const bool ok = h >= 0 && h < p.H && w >= 0 && w < p.W;
+        v[kh * K + kw] = ok ? __ldg(reinterpret_cast<const float4*>(in + (h * p.W + w) * p.in_ldc))
+                            : make_float4(-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX);
+      }
+    float4 m = v[0];
+#pragma unroll
+    for (int j = 1; j < K * K; ++j) m = max4(m, v[j]);
+    *reinterpret_cast<float4*>(p.out_ptrs[n] + p.out_off + (ho * p.Wo + wo) * p.out_ldc + c4 * 4) = m;
+  }
+}
+
 // Row-sliding max-pool (k <= 3): a thread owns one output row of 4 channels
 // and walks it left to right; each input column's k-row maximum is computed
 // once and kept in a 3-entry ring, so a stride-1 3x3 pool loads every input
@@ -197,10 +231,15 @@ cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {
   const long rows = static_cast<long>(p.nimg) * p.Ho * (p.C / 4);
   // The row-sliding form loads each input once per row but serialises a
   // row's outputs; it pays only when rows alone fill the GPU several times.
+  const long outs = static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4);
   if (p.stride == 1 && rows >= 148L * 2048 * 2)
     maxpool_rows_kernel<<<grid_for(rows), kThreads, 0, s>>>(p);
+  else if (p.k == 3)
+    maxpool_unrolled_kernel<3><<<grid_for(outs), kThreads, 0, s>>>(p);
+  else if (p.k == 2)
+    maxpool_unrolled_kernel<2><<<grid_for(outs), kThreads, 0, s>>>(p);
   else
-    maxpool_kernel<<<grid_for(static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4)), kThreads, 0, s>>>(p);
+    maxpool_kernel<<<grid_for(outs), kThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
