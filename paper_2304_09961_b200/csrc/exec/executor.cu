@@ -93,6 +93,47 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
         throw std::runtime_error("cuTensorMapEncodeTiled failed for " + op.name);
     }
   }
+  // Window mode for spatial convs (opt-in, BS_CONV_WIN=1; measured slower
+  // than the cp.async gather on B200): the
+  // weights are re-laid chunk-major into their own pool, and each conv gets a
+  // window tensor map over the slot space.
+  const char* win_env = std::getenv("BS_CONV_WIN");
+  const bool use_win = win_env && win_env[0] == '1';
+  wins_.resize(suite_.nets.size());
+  {
+    std::vector<float> pool;
+    std::vector<std::pair<std::size_t, std::size_t>> where;  // (net, op) of each window conv
+    for (std::size_t n = 0; n < suite_.nets.size() && use_win; ++n) {
+      const NetDef& net = suite_.nets[n];
+      wins_[n].resize(net.ops.size());
+      for (std::size_t i = 0; i < net.ops.size(); ++i) {
+        const OpDef& op = net.ops[i];
+        if (op.kind != OpKind::conv) continue;
+        WinMap& wm = wins_[n][i];
+        if (!conv_window_geometry(op.in.C, op.KH, op.KW, op.Ho, op.Wo, op.stride, &wm.geom)) continue;
+        wm.w_off = pool.size();
+        pool.resize(pool.size() + static_cast<std::size_t>(op.out.C) * wm.geom.Kwin);
+        conv_window_weights(suite_.weights.data() + op.w_off, op.out.C, op.Kpad, op.KH, op.KW, op.in.C, wm.geom,
+                            pool.data() + wm.w_off);
+        where.emplace_back(n, i);
+      }
+    }
+    if (!pool.empty()) {
+      ck(cudaMalloc(&d_win_weights_, pool.size() * sizeof(float)), "window weights");
+      ck(cudaMemcpy(d_win_weights_, pool.data(), pool.size() * sizeof(float), cudaMemcpyHostToDevice),
+         "window weights H2D");
+    }
+    for (const auto& [n, i] : where) {
+      const NetDef& net = suite_.nets[n];
+      const OpDef& op = net.ops[i];
+      const TensorDef& ti = net.tensors[static_cast<std::size_t>(op.in.t)];
+      WinMap& wm = wins_[n][i];
+      wm.ok = encode_weight_map(&wm.wmap, d_win_weights_ + wm.w_off, op.out.C, wm.geom.Kwin) &&
+              encode_window_map(&wm.amap, arena_ + ti.off + op.in.coff, op.in.C, ti.W, ti.H, ti.C, total_slots_,
+                                static_cast<long>(slot_floats_), wm.geom);
+      if (!wm.ok) throw std::runtime_error("window tensor maps failed for " + op.name);
+    }
+  }
   // One activation tensor map per conv input (the slot space never moves).
   // BS_CONV_TMA=1: feed conv activations by TMA boxes wherever the geometry
   // allows (default: cp.async gather; see DESIGN.md §4 for the ingest limits).
@@ -134,6 +175,7 @@ Executor::~Executor() {
     cudaFree(w->counters);
   }
   cudaFree(d_weights_);
+  cudaFree(d_win_weights_);
   cudaFree(arena_);
   cudaFree(scratch_ptrs_);
   cudaFree(flush_);
@@ -225,7 +267,10 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
       {
         const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
         const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
-        if (ni < amaps_.size() && oi < amaps_[ni].size() && amaps_[ni][oi].ok)
+        if (ni < wins_.size() && oi < wins_[ni].size() && wins_[ni][oi].ok)
+          conv_use_window(p, wins_[ni][oi].amap, wins_[ni][oi].wmap, wins_[ni][oi].geom, arena_,
+                          static_cast<long>(slot_floats_), total_slots_);
+        else if (ni < amaps_.size() && oi < amaps_[ni].size() && amaps_[ni][oi].ok)
           conv_use_act_map(p, amaps_[ni][oi].map, amaps_[ni][oi].geom, arena_, static_cast<long>(slot_floats_),
                            total_slots_);
       }

@@ -163,6 +163,14 @@ class Executor {
     bool ok = false;
   };
   std::vector<std::vector<ActMap>> amaps_;        // [net][op] conv input maps over the slot space
+  struct WinMap {
+    CUtensorMap amap{}, wmap{};
+    WinGeom geom;
+    std::size_t w_off = 0;  // into d_win_weights_
+    bool ok = false;
+  };
+  std::vector<std::vector<WinMap>> wins_;         // [net][op] window-mode maps (spatial convs)
+  float* d_win_weights_ = nullptr;                // chunk-major copies of the spatial conv weights
   long total_slots_ = 0;
   ConvWorkspace conv_ws_;                         // split-K partials + tile counters (serving stream)
   ConvWorkspace side_ws_;                         // the same for the client-prefix side stream

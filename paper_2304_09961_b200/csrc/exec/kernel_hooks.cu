@@ -23,6 +23,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
   const size_t in_img = static_cast<size_t>(d->H) * d->W * d->in_ldc;
   const size_t out_img = static_cast<size_t>(d->Ho) * d->Wo * d->out_ldc;
   const size_t res_img = res_host ? static_cast<size_t>(d->Ho) * d->Wo * d->res_ldc : 0;
+  float *dwin = nullptr;
   float *din = nullptr, *dw = nullptr, *db = nullptr, *dout = nullptr, *dres = nullptr;
   float** ptrs = nullptr;
   ConvWorkspace ws;
@@ -74,7 +75,23 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_off = d->out_coff;
     p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_off = d->res_coff;
     p.relu = d->relu; p.round_out = d->round_out; p.split = d->split;
-    {
+    WinGeom wg;
+    const char* win_env = std::getenv("BS_CONV_WIN");
+    if (win_env && win_env[0] == '1' && conv_window_geometry(d->Cin, d->KH, d->KW, d->Ho, d->Wo, d->stride, &wg)) {
+      // Window mode: chunk-major weights + window map over the nimg images.
+      std::vector<float> hw(static_cast<size_t>(d->N) * wg.Kwin);
+      conv_window_weights(w_host, d->N, Kpad, d->KH, d->KW, d->Cin, wg, hw.data());
+      CK(cudaMalloc(&dwin, hw.size() * sizeof(float)));
+      CK(cudaMemcpy(dwin, hw.data(), hw.size() * sizeof(float), cudaMemcpyHostToDevice));
+      CUtensorMap amap, wmap;
+      if (!encode_window_map(&amap, din + d->in_coff, d->Cin, d->W, d->H, d->in_ldc, nimg, static_cast<long>(in_img),
+                             wg) ||
+          !encode_weight_map(&wmap, dwin, d->N, wg.Kwin)) {
+        rc = bs_fail(BS_ECUDA, "window tensor maps failed");
+        goto done;
+      }
+      conv_use_window(p, amap, wmap, wg, din, static_cast<long>(in_img), nimg);
+    } else {
       // TMA activation path: the nimg input images are the slot space.
       ActGeom g;
       CUtensorMap amap;
@@ -90,18 +107,18 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     }
     unsigned long long* trace = nullptr;
     if (std::getenv("BS_CONV_TRACE")) {
-      CK(cudaMalloc(&trace, 8 * 1400));
-      CK(cudaMemset(trace, 0, 8 * 1400));
+      CK(cudaMalloc(&trace, 8 * 2400));
+      CK(cudaMemset(trace, 0, 8 * 2400));
       p.trace = trace;
       CK(launch_conv_tc(p, ws, 0));  // warm-up (TMEM/TMA descriptors, L2)
       CK(cudaDeviceSynchronize());
-      CK(cudaMemset(trace, 0, 8 * 1400));
+      CK(cudaMemset(trace, 0, 8 * 2400));
     }
     CK(launch_conv_tc(p, ws, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));
     if (trace) {
-      unsigned long long h[1400];
+      unsigned long long h[2400];
       CK(cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost));
       unsigned long long t0 = ~0ULL;
       for (int b = 0; b < 254; ++b)
@@ -112,9 +129,10 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
           std::fprintf(stderr, "  cta %3d start %7lld setup %7lld firstA %7lld end %7lld\n", b, rel(h[8 + 4 * b]),
                        rel(h[9 + 4 * b]), rel(h[10 + 4 * b]), rel(h[11 + 4 * b]));
       for (int it = 0; it < 48 && h[1024 + it * 5 + 4]; ++it)
-        std::fprintf(stderr, "  it %2d A %7lld B %7lld landed %7lld split %7lld mma %7lld\n", it,
+        std::fprintf(stderr, "  it %2d A %7lld B %7lld landed %7lld split %7lld mma %7lld | cvt %7lld slot %7lld st %7lld wst %7lld\n", it,
                      rel(h[1024 + it * 5]), rel(h[1025 + it * 5]), rel(h[1026 + it * 5]), rel(h[1027 + it * 5]),
-                     rel(h[1028 + it * 5]));
+                     rel(h[1028 + it * 5]), rel(h[2048 + it * 4]), rel(h[2049 + it * 4]), rel(h[2050 + it * 4]),
+                     rel(h[2051 + it * 4]));
       p.trace = nullptr;
       cudaFree(trace);
     }
@@ -135,7 +153,7 @@ done:
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
   cudaFree(ws.partials); cudaFree(ws.counters);
-  cudaFree(din); cudaFree(dw); cudaFree(db); cudaFree(dout); cudaFree(dres); cudaFree(ptrs);
+  cudaFree(din); cudaFree(dw); cudaFree(dwin); cudaFree(db); cudaFree(dout); cudaFree(dres); cudaFree(ptrs);
   return rc;
 }
 

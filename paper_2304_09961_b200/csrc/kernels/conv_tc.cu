@@ -106,6 +106,68 @@ bool encode_act_map(CUtensorMap* map, const float* base, int C, int W, int H, in
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool conv_window_geometry(int Cin, int KH, int KW, int Ho, int Wo, int stride, WinGeom* wg) {
+  if (KH * KW <= 1) return false;
+  WinGeom w;
+  if (!conv_act_geometry(Cin, Ho, Wo, stride, &w.act)) return false;
+  const int g = Cin % 32 == 0 ? 32 : (Cin == 4 || Cin == 8 || Cin == 16) ? Cin : 0;
+  if (!g) return false;
+  w.act.g = g;
+  w.Win = (Wo - 1) * stride + KW;
+  w.Hin = (w.act.Hb - 1) * stride + KH;
+  if (w.Win > 256 || w.Hin > 256) return false;
+  w.ktpc = (KH * KW * g + conv_tc::kBK - 1) / conv_tc::kBK;
+  w.Kwin = (Cin / g) * w.ktpc * conv_tc::kBK;
+  w.tx_bytes = w.Win * w.Hin * g * 4;
+  w.img_bytes = (w.tx_bytes + 1023) / 1024 * 1024;
+  if (w.act.G * w.img_bytes > conv_tc::kWinBytes) return false;
+  *wg = w;
+  return true;
+}
+
+void conv_window_weights(const float* w, int N, int Kpad_src, int KH, int KW, int Cin, const WinGeom& wg,
+                         float* out) {
+  const int g = wg.act.g, taps = KH * KW, tpk_total = wg.ktpc * conv_tc::kBK / g;
+  for (int n = 0; n < N; ++n) {
+    float* o = out + static_cast<std::size_t>(n) * wg.Kwin;
+    const float* src = w + static_cast<std::size_t>(n) * Kpad_src;
+    for (int c = 0; c < Cin / g; ++c)
+      for (int t = 0; t < tpk_total; ++t)
+        for (int ci = 0; ci < g; ++ci)
+          o[(c * tpk_total + t) * g + ci] = t < taps ? src[t * Cin + c * g + ci] : 0.f;
+  }
+}
+
+bool encode_window_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
+                       long slot_floats, const WinGeom& wg) {
+  const EncodeTiledFn encode = encode_fn();
+  if (!encode || (reinterpret_cast<uintptr_t>(base) & 15) || ldc % 4 || slot_floats % 4) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(slots)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ldc) * 4, static_cast<cuuint64_t>(W) * ldc * 4,
+                                 static_cast<cuuint64_t>(slot_floats) * 4};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(wg.act.g), static_cast<cuuint32_t>(wg.Win),
+                             static_cast<cuuint32_t>(wg.Hin), 1};
+  const cuuint32_t elem[4] = {1, 1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, elem,
+                CU_TENSOR_MAP_INTERLEAVE_NONE,
+                wg.act.g == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void conv_use_window(ConvParams& p, const CUtensorMap& amap, const CUtensorMap& wmap, const WinGeom& wg,
+                     const float* slot_base, long slot_floats, long slots) {
+  conv_use_act_map(p, amap, wg.act, slot_base, slot_floats, slots);
+  p.wmap = wmap;
+  p.a_win = 1;
+  p.Win = wg.Win;
+  p.Hin = wg.Hin;
+  p.ktpc = wg.ktpc;
+  p.win_img_bytes = wg.img_bytes;
+  p.win_tx_bytes = wg.tx_bytes;
+  p.Kpad = wg.Kwin;
+}
+
 void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& g, const float* slot_base,
                       long slot_floats, long slots) {
   p.amap = map;
@@ -127,6 +189,9 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   const int sms = sm_count();
   const int KT = p.Kpad / conv_tc::kBK;
   if (p.a_tma && (p.G < 1 || p.G > 4 || p.Wb * p.Hb * p.G != conv_tc::kBM || p.a_g % 4 || p.Cin % p.a_g))
+    return cudaErrorInvalidValue;
+  if (p.a_win && (!p.a_tma || p.G * p.win_img_bytes > conv_tc::kWinBytes || p.ktpc <= 0 ||
+                  p.Kpad != (p.Cin / p.a_g) * p.ktpc * conv_tc::kBK))
     return cudaErrorInvalidValue;
   p.m_tiles = p.a_tma ? (p.G == 1 ? p.nimg * p.tpi : (p.nimg + p.G - 1) / p.G)
                       : (p.nimg * p.Ho * p.Wo + conv_tc::kBM - 1) / conv_tc::kBM;
@@ -165,8 +230,8 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   const int grid = std::min(units, sms);
   static const bool log = std::getenv("BS_CONV_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d tma=%d box=%dx%dx%d g=%d\n",
-                 p.nimg * p.Ho * p.Wo, p.N, p.K, KT, bn, tiles, p.ksplits, grid, p.a_tma, p.Hb, p.Wb, p.G, p.a_g);
+    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d tma=%d win=%d box=%dx%dx%d g=%d\n",
+                 p.nimg * p.Ho * p.Wo, p.N, p.K, KT, bn, tiles, p.ksplits, grid, p.a_tma, p.a_win, p.Hb, p.Wb, p.G, p.a_g);
   if (p.split) {
     if (bn == 32) return launch_bn<32, true>(p, grid, stream);
     if (bn == 64) return launch_bn<64, true>(p, grid, stream);

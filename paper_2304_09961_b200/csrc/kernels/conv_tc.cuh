@@ -32,9 +32,10 @@
 //     two MMAs per K step and no extra HBM or shared-memory traffic (A_lo
 //     lives in TMEM next to A_hi).
 //
-// Warp roles: 0-3 A cp.async producers (or, with TMA activations, a second
+// Warp roles: 0-3 A cp.async producers (or, with TMA activations, the second
 // converter group), 4-7 epilogue (TMEM lanes 0-127), 8 MMA issuer (+ TMEM
-// owner), 9 B TMA issuer, 10-13 A converters, 14 A TMA issuer.
+// owner), 9 B TMA issuer, 10-13 A converters (group 0), 14 A TMA issuer,
+// 15-18 A converters (group 1, cp.async gather).
 #pragma once
 #include <cstdint>
 
@@ -83,6 +84,15 @@ struct ConvParams {
   const float* slot_base;       // slot index of an image = (in_ptrs[i] - slot_base) / slot_floats
   long slot_floats;
   int oob_slot;                 // a slot coordinate past the map (zero-filled boxes)
+  // Window mode (a_win = 1, spatial convs; implies a_tma): per M tile and
+  // channel chunk of g, one TMA box brings the input window Hin x Win x g of
+  // each image; converter warps expand the im2col rows of all taps from it.
+  // K order is chunk-major ((chunk, tap, ci), ktpc K tiles per chunk, padded
+  // taps zero) and the weights (wmap) are laid out to match.
+  int a_win;
+  int Win, Hin, ktpc;
+  int win_img_bytes;            // smem stride between the G image windows (1024-aligned)
+  int win_tx_bytes;             // bytes one image window box delivers
 };
 
 // Device workspace for split-K (owned by the caller; counters zeroed once).
@@ -97,6 +107,7 @@ namespace conv_tc {
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // fp32 elements per 128-byte K row
+constexpr int kWinBytes = 65536;  // one input window (window mode); two share the raw A ring
 
 // Pipeline geometry per N tile. Three rings decouple the stages so no load
 // waits on an MMA it does not feed:
@@ -108,12 +119,16 @@ constexpr int kBK = 32;  // fp32 elements per 128-byte K row
 //          tensor core.
 template <int BN, bool SPLIT>
 struct Cfg {
-  static constexpr int kThreads = 480;
+  static constexpr int kThreads = 608;
   static constexpr int RA = BN == 32 ? 10 : 8;
-  static constexpr int NB = BN == 128 ? 5 : 8;
   static constexpr int kACols = SPLIT ? 2 * kBK : kBK;          // TMEM columns per A slot
   static constexpr int kTA0 = 2 * BN;                            // first A column (after 2 accumulators)
-  static constexpr int TA = (512 - kTA0) / kACols < 8 ? (512 - kTA0) / kACols : 8;
+  // One operand stage = (TMEM A slot, B smem stage), released by a single
+  // tcgen05.commit per K tile (each commit costs the tensor pipe ~84 cycles).
+  static constexpr int kTAmax = (512 - kTA0) / kACols;
+  static constexpr int kNBmax = (232448 - 1024 - 512 - RA * kBM * 128 - kBM * 32 * 4) / (BN * 128);
+  static constexpr int TA = kTAmax < kNBmax ? (kTAmax < 8 ? kTAmax : 8) : (kNBmax < 8 ? kNBmax : 8);
+  static constexpr int NB = TA;
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kBOffset = RA * kABytes;
@@ -122,6 +137,7 @@ struct Cfg {
   static constexpr int kTotal = kBarOffset + 512 + 1024;        // barriers + alignment slack
   static_assert(kTotal <= 232448, "shared memory budget");
   static_assert(TA >= 2, "TMEM budget");
+  static_assert(RA * kABytes >= 2 * kWinBytes, "window ring");
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -181,6 +197,22 @@ __device__ __forceinline__ bool row_pixel(const ConvParams& p, int mt, int r, in
   return img < p.nimg && h < p.Ho && dw < p.Wo;
 }
 
+// A operand conversion. 2xTF32: hi = x with the 13 low mantissa bits
+// cleared (exactly TF32), lo = x - hi (exact in fp32; the tensor core keeps
+// its top 11 bits, so |error| <= 2^-21 |x|). Plain TF32: round to nearest
+// (ties away) by integer add + mask, valid for finite x.
+template <bool SPLIT>
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  const uint32_t u = __float_as_uint(x);
+  if constexpr (SPLIT) {
+    hi = u & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
+  } else {
+    hi = (u + 0x1000u) & 0xffffe000u;
+    (void)lo;
+  }
+}
+
 __device__ __forceinline__ float epilogue_op(const ConvParams& p, float x, int n, const float* res_row) {
   if (p.bias) x += __ldg(p.bias + n);
   if (res_row) x += res_row[n];
@@ -201,12 +233,14 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
   uint64_t* ra_full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
   uint64_t* ra_empty = ra_full + RA;
   uint64_t* b_full = ra_empty + RA;
-  uint64_t* b_empty = b_full + NB;
-  uint64_t* ta_full = b_empty + NB;
+  uint64_t* ta_full = b_full + NB;
   uint64_t* ta_empty = ta_full + TA;
+  uint64_t* b_empty = ta_empty;        // same ring: one commit frees slot and stage
   uint64_t* acc_full = ta_empty + TA;  // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* win_full = acc_empty + 2;  // [2] window mode
+  uint64_t* win_empty = win_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(win_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -225,7 +259,6 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     }
     for (int s = 0; s < NB; ++s) {
       ptx::mbar_init(&b_full[s], 1);
-      ptx::mbar_init(&b_empty[s], 1);
     }
     for (int s = 0; s < TA; ++s) {
       ptx::mbar_init(&ta_full[s], 128);
@@ -234,6 +267,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
       ptx::mbar_init(&acc_empty[a], 128);
+      ptx::mbar_init(&win_full[a], 1);
+      ptx::mbar_init(&win_empty[a], 256);  // both converter groups, once per window
     }
     ptx::fence_mbar_init();
   }
@@ -251,6 +286,117 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
   // TMEM lane: rn_tf32(a) (+ the residual a - rn_tf32(a) for 2xTF32). With
   // TMA activations two converter groups (warps 10-13 and 0-3) take
   // alternate K tiles so the conversion latency overlaps.
+  // Images of an M tile (TMA geometry): slot index and first output row.
+  auto tile_slots = [&](const Unit& w, int (&slot)[4], int (&h0)[4]) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      int img;
+      if (p.G == 1) {
+        img = w.mt / p.tpi;
+        h0[b] = (w.mt - img * p.tpi) * p.Hb;
+      } else {
+        img = w.mt * p.G + b;
+        h0[b] = 0;
+      }
+      slot[b] = (b < p.G && img < p.nimg) ? static_cast<int>((p.in_ptrs[img] - p.slot_base) / p.slot_floats)
+                                          : p.oob_slot;
+    }
+  };
+
+  // Window-mode converter: the same TMEM hand-off as convert(), but the 32
+  // K values of a row are read from the chunk's input window (taps of one
+  // channel chunk), so each input element enters the SM once per M tile.
+  auto convert_window = [&](int group, int ngroups, int trace_tid) {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int R = kBM / p.G;
+    const int b = row / R, rr = row - b * R;
+    const int dh = rr / p.Wb;
+    const int dw = min(rr - dh * p.Wb, p.Wo - 1);  // padding columns re-read a valid pixel
+    const int pix0 = dh * p.stride * p.Win + dw * p.stride;
+    const uint32_t win0 = smem_base + static_cast<uint32_t>(b * p.win_img_bytes);
+    const int g = p.a_g, tpk = kBK / g, taps = p.KH * p.KW;
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + S::kTA0;
+    int it = 0, wi = -1;
+    bool waited = false;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = unit_of(p, u, BN, KT);
+      for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+        const int c = kt / p.ktpc, jt = kt - c * p.ktpc;
+        if (kt == w.kt0 || jt == 0) {
+          ++wi;
+          waited = false;
+        }
+        const uint32_t win = win0 + static_cast<uint32_t>((wi & 1) * kWinBytes);
+        if (it % ngroups == group) {
+          if (!waited) {
+            ptx::mbar_wait(&win_full[wi & 1], (wi >> 1) & 1);
+            waited = true;
+          }
+          if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 2] = gtime();
+          float4 v[8];
+          if (g == kBK) {
+            const int t = jt;
+            if (t < taps) {
+              const int kh = t / p.KW, kw = t - kh * p.KW;
+              const int pix = pix0 + kh * p.Win + kw;
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc) v[cc] = ptx::lds128(win + swz(pix, cc));
+            } else {
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc) v[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          } else {
+            const int cpt = g / 4;  // 16-byte chunks per tap
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+              const int j = cc / cpt, c4 = cc - j * cpt;
+              const int t = jt * tpk + j;
+              if (t < taps) {
+                const int kh = t / p.KW, kw = t - kh * p.KW;
+                v[cc] = ptx::lds128(win + (pix0 + kh * p.Win + kw) * (g * 4) + c4 * 16);
+              } else {
+                v[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+            }
+          }
+          uint32_t hi[32];
+          [[maybe_unused]] uint32_t lo[32];
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const float x[4] = {v[cc].x, v[cc].y, v[cc].z, v[cc].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) split_tf32<SPLIT>(x[e], hi[4 * cc + e], lo[4 * cc + e]);
+          }
+          const int sa = it % TA;
+          const bool tr = p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48;
+          if (tr) p.trace[2048 + it * 4 + 0] = gtime();
+          if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
+          if (tr) p.trace[2048 + it * 4 + 1] = gtime();
+          ptx::tc_fence_after();
+          const uint32_t dst = lane_base + sa * S::kACols;
+          ptx::tmem_st32(dst, hi);
+          if constexpr (SPLIT) ptx::tmem_st32(dst + kBK, lo);
+          if (tr) p.trace[2048 + it * 4 + 2] = gtime();
+          ptx::tmem_st_wait();
+          if (tr) p.trace[2048 + it * 4 + 3] = gtime();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&ta_full[sa]);
+          if (tr) p.trace[1024 + it * 5 + 3] = gtime();
+        }
+        if (jt == p.ktpc - 1 || kt == w.kt1 - 1) {
+          // Done with this window (own reads complete); waiting for its fill
+          // first keeps the arrival in the window's own release phase.
+          if (!waited) {
+            ptx::mbar_wait(&win_full[wi & 1], (wi >> 1) & 1);
+            waited = true;
+          }
+          ptx::mbar_arrive(&win_empty[wi & 1]);
+        }
+      }
+    }
+  };
+
   auto convert = [&](int group, int ngroups, int trace_tid) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
@@ -287,11 +433,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
         for (int c = 0; c < 8; ++c) {
           const float x[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float h = ptx::round_tf32(x[e]);
-            hi[4 * c + e] = __float_as_uint(h);
-            if constexpr (SPLIT) lo[4 * c + e] = __float_as_uint(x[e] - h);
-          }
+          for (int e = 0; e < 4; ++e) split_tf32<SPLIT>(x[e], hi[4 * c + e], lo[4 * c + e]);
         }
         const int sa = it % TA;
         if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
@@ -307,15 +449,38 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     }
   };
 
-  if (warp < 4 && p.a_tma) {
+  if (warp < 4 && p.a_win) {
+    convert_window(1, 2, 0);
+  } else if (warp < 4 && p.a_tma) {
     convert(1, 2, 0);
   } else if (warp == 14) {
+    if (p.a_win && lane == 0) {
+      // ------------------------------------------ input windows by TMA
+      int wi = -1, it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = unit_of(p, u, BN, KT);
+        int slot[4], h0[4];
+        tile_slots(w, slot, h0);
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+          const int c = kt / p.ktpc, jt = kt - c * p.ktpc;
+          if (kt != w.kt0 && jt != 0) continue;
+          if (p.trace && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
+          ++wi;
+          if (wi >= 2) ptx::mbar_wait(&win_empty[wi & 1], ((wi >> 1) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&win_full[wi & 1], static_cast<uint32_t>(p.G * p.win_tx_bytes));
+          const uint32_t win = smem_base + static_cast<uint32_t>((wi & 1) * kWinBytes);
+          for (int b = 0; b < p.G; ++b)
+            ptx::tma_load_4d(win + b * p.win_img_bytes, &p.amap, c * p.a_g, -p.pad, h0[b] * p.stride - p.pad,
+                             slot[b], &win_full[wi & 1]);
+        }
+      }
+    }
     // ------------------------------------------------------ A by TMA boxes
     // K tile kt = 32 / g boxes per image of the tile: k = kt * 32 + j * g
     // -> (tap, ci); box origin = (ci, w0 * s - pad + kw, h0 * s - pad + kh,
     // slot). Boxes past K or past the batch are aimed outside the map so the
     // stage is zero-filled and the byte count stays constant.
-    if (p.a_tma && lane == 0) {
+    else if (p.a_tma && lane == 0) {
       const int R = kBM / p.G;
       const int pieces = kBK / p.a_g;
       const uint32_t box_bytes = static_cast<uint32_t>(R * p.a_g * 4);
@@ -323,20 +488,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit w = unit_of(p, u, BN, KT);
         int slot[4], h0[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          int img;
-          if (p.G == 1) {
-            img = w.mt / p.tpi;
-            h0[b] = (w.mt - img * p.tpi) * p.Hb;
-          } else {
-            img = w.mt * p.G + b;
-            h0[b] = 0;
-          }
-          slot[b] = (b < p.G && img < p.nimg)
-                        ? static_cast<int>((p.in_ptrs[img] - p.slot_base) / p.slot_floats)
-                        : p.oob_slot;
-        }
+        tile_slots(w, slot, h0);
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % RA;
           if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
@@ -638,8 +790,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
             ptx::mma_tf32_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
             if constexpr (SPLIT) ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
           }
-          ptx::mma_commit(&ta_empty[sa]);
-          ptx::mma_commit(&b_empty[sb]);
+          ptx::mma_commit(&ta_empty[sa]);  // == b_empty[sb]
           if (kt == w.kt1 - 1) ptx::mma_commit(&acc_full[acc]);
         }
         __syncwarp();
@@ -662,7 +813,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     }
     __syncwarp();
   } else if (warp >= 10 && warp < 14) {
-    convert(0, p.a_tma ? 2 : 1, 320);
+    if (p.a_win) convert_window(0, 2, 320);
+    else convert(0, 2, 320);
+  } else if (warp >= 15 && warp < 19 && !p.a_win && !p.a_tma) {
+    convert(1, 2, 480);
   }
 
   ptx::tc_fence_before();
@@ -694,6 +848,24 @@ bool conv_act_geometry(int Cin, int Ho, int Wo, int stride, ActGeom* geom);
 // {1, stride, stride, 1}; 128B swizzle when g == 32.
 bool encode_act_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
                     long slot_floats, const ActGeom& geom, int stride);
+// Window mode for a KH x KW (> 1) conv: channel chunk g = 32 (or Cin when
+// Cin is 4, 8 or 16), window Hin x Win per image, ktpc K tiles per chunk and
+// the chunk-major K extent Kwin. False when the window does not fit a 64 KB
+// buffer (the conv then uses the gather paths).
+struct WinGeom {
+  ActGeom act;
+  int Win = 0, Hin = 0, ktpc = 0, Kwin = 0, img_bytes = 0, tx_bytes = 0;
+};
+bool conv_window_geometry(int Cin, int KH, int KW, int Ho, int Wo, int stride, WinGeom* wg);
+// Chunk-major copy of a [N][Kpad_src] (tap-major K = (kh, kw, ci)) weight
+// matrix: out[N][Kwin].
+void conv_window_weights(const float* w, int N, int Kpad_src, int KH, int KW, int Cin, const WinGeom& wg,
+                         float* out);
+// Window tensor map: {C, W, H, slot} box {g, Win, Hin, 1}.
+bool encode_window_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
+                       long slot_floats, const WinGeom& wg);
+void conv_use_window(ConvParams& p, const CUtensorMap& amap, const CUtensorMap& wmap, const WinGeom& wg,
+                     const float* slot_base, long slot_floats, long slots);
 // Fills the TMA fields of p (a_tma = 1) from a geometry and an encoded map.
 void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& geom, const float* slot_base,
                       long slot_floats, long slots);

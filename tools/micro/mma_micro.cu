@@ -13,12 +13,12 @@ __global__ void k(long long* out, int iters) {
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbar_init(); }
-  if (warp == 0) ptx::tmem_alloc<256>(&slot);
+  if (warp == 0) ptx::tmem_alloc<512>(&slot);
   ptx::tc_fence_before(); __syncthreads(); ptx::tc_fence_after();
   const uint32_t tmem = slot;
   const uint32_t a = ptx::smem_u32(smem), b = a + 16384;
   const uint64_t ad = ptx::sw128_kmajor_desc(a), bd = ptx::sw128_kmajor_desc(b);
-  constexpr uint32_t idesc = KIND == 0 ? ptx::make_idesc(2, 128, N) : ptx::make_idesc(1, 128, N);
+  constexpr uint32_t idesc = KIND != 1 ? ptx::make_idesc(2, 128, N) : ptx::make_idesc(1, 128, N);
   long long t0 = 0, t1 = 0;
   if (warp == 0) {
     uint32_t phase = 0;
@@ -27,7 +27,8 @@ __global__ void k(long long* out, int iters) {
       if (lane == 0) {
         for (int kk = 0; kk < 4; ++kk) {
           if (KIND == 0) ptx::mma_tf32(tmem, ad + 2 * kk, bd + 2 * kk, idesc, (it | kk) != 0);
-          else ptx::mma_f16(tmem, ad + 2 * kk, bd + 2 * kk, idesc, (it | kk) != 0);
+          else if (KIND == 1) ptx::mma_f16(tmem, ad + 2 * kk, bd + 2 * kk, idesc, (it | kk) != 0);
+          else ptx::mma_tf32_ts(tmem, tmem + 256 + 8 * kk, bd + 2 * kk, idesc, (it | kk) != 0);
         }
         if (MODE >= 1) ptx::mma_commit(&bar);
       }
@@ -42,7 +43,7 @@ __global__ void k(long long* out, int iters) {
     if (lane == 0) out[blockIdx.x] = t1 - t0;
   }
   ptx::tc_fence_before(); __syncthreads();
-  if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc<256>(tmem); }
+  if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc<512>(tmem); }
 }
 
 template <int N, int MODE, int KIND>
@@ -67,5 +68,9 @@ int main() {
   run<128, 0, 1>("bf16 4 MMAs(K=16)/group, one commit", 256);
   run<128, 2, 1>("bf16 4 MMAs + commit + wait per group", 256);
   run<256, 0, 1>("bf16 4 MMAs(K=16)/group, one commit", 256);
+  run<128, 0, 2>("tf32 TS (A in TMEM) 4 MMAs/group, one commit", 256);
+  run<128, 1, 2>("tf32 TS 4 MMAs + commit per group", 256);
+  run<128, 2, 2>("tf32 TS 4 MMAs + commit + wait per group", 256);
+  run<64, 0, 2>("tf32 TS (A in TMEM) 4 MMAs/group, one commit", 256);
   return 0;
 }
