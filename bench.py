@@ -134,27 +134,62 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# BASELINE.json configs measured live (config 5, collaborative offload, runs
+# in replay only: its client side is modelled, tests/test_executor_gpu.py).
+CONFIGS = {
+    1: {"suite": "small_cnn", "max_batch": 10, "process": "constant", "scheduler": "ours-time",
+        "granularity": "request",
+        "workload": "config 1: SmallCNN 32x32 single DNN, Constant arrivals, completion-time DP (Ours-Time), "
+                    "request granularity, B=10"},
+    2: {"suite": "googlenet", "max_batch": 90, "process": "poisson", "scheduler": "ours-tardy",
+        "granularity": "layer",
+        "workload": "config 2: GoogLeNet 224x224 single DNN, Poisson arrivals, Our-Tardy (on-time objective), "
+                    "partial batching at layer granularity, B=90, 1 server per GPU"},
+    3: {"suite": "resnet50_pair", "max_batch": 90, "process": "pareto", "scheduler": "ours-time",
+        "granularity": "group", "shared_batching": True,
+        "workload": "config 3: two DNNs sharing a ResNet-50 backbone (heads 1000 / 365 classes), shared-layer "
+                    "merge batching with riders, Pareto arrivals (alpha 1.25), G=5, B=90"},
+    4: {"suite": "hetero3", "max_batch": 90, "process": "poisson", "scheduler": "ours-time",
+        "granularity": "group",
+        "workload": "config 4: GoogLeNet + ResNet-50 + MobileNetV2 (no shared layers), equal Poisson mix, "
+                    "multi-DNN permutation DP, G=5, B=90, request streams sharded over GPUs"},
+}
+
+
 def run_ours(a, ws, rank, local) -> dict | None:
     from paper_2304_09961_b200.executor import Executor
 
+    cfg = CONFIGS[a.config]
     pk = peaks()
-    ex = Executor("googlenet", device=local, max_batch=90, max_requests=a.slots)
+    mb = cfg["max_batch"]
+    ex = Executor(cfg["suite"], device=local, max_batch=mb, max_requests=a.slots)
     ex.set_precision(a.precision)
-    prof = ex.profile_table(batches=BATCHES, reps=10)
-    layers = prof["components"][0]["layers"]
-    t1 = sum(dict(L["runtime_ms"])[1] for L in layers)
-    t90 = sum(dict(L["runtime_ms"])[90] for L in layers)
-    # Fixed target: 5 ms = 6.25 x 0.8 ms, the best single-request GoogLeNet
-    # latency measured on this B200 build (SURVEY.md §8d sets D = 6.25 x T1,
-    # the paper's 150 ms / 24 ms ratio). It is a constant so that a kernel
-    # change cannot move the target; the current T1 is reported beside it.
-    deadline = a.deadline_ms
-    base = {"profile": prof, "sim": {"scheduler": "ours-tardy", "granularity": "layer", "max_batch": 90},
-            "image_pool": 64, "pipeline_depth": 2}
+    prof = ex.profile_table(batches=[b for b in BATCHES if b < mb] + [mb], reps=10)
+    names = [n["name"] for n in ex.desc["nets"]]
+    comp = {c["id"]: c for c in prof["components"]}
+
+    def dnn_ms(d, b):
+        return sum(dict(L["runtime_ms"])[b] for cid in d["stages"] for L in comp[cid]["layers"])
+
+    t1 = max(dnn_ms(d, 1) for d in prof["dnns"])
+    tmax = max(dnn_ms(d, mb) for d in prof["dnns"])
+    # Config 2 keeps a fixed 5 ms target (= 6.25 x 0.8 ms, the best
+    # single-request GoogLeNet latency measured on this build; SURVEY.md §8d
+    # sets D = 6.25 x T1, the paper's 150 ms / 24 ms ratio) so that a kernel
+    # change cannot move the target. Other configs use D = 6.25 x T1 of their
+    # slowest DNN, measured at startup.
+    deadline = a.deadline_ms if a.config == 2 else round(6.25 * t1, 3)
+    sim = {"scheduler": cfg["scheduler"], "granularity": cfg["granularity"], "max_batch": mb}
+    if "shared_batching" in cfg:
+        sim["shared_batching"] = cfg["shared_batching"]
+    base = {"profile": prof, "sim": sim, "image_pool": 64, "pipeline_depth": 2}
 
     def job(rate, count, seed, h2d=False):
-        return dict(base, workload={"process": "poisson", "rate": rate, "count": count, "seed": seed,
-                                    "relative_deadline": deadline}, h2d=h2d)
+        w = {"process": cfg["process"], "rate": rate, "count": count, "seed": seed, "relative_deadline": deadline}
+        if len(names) > 1:
+            w["dnn_mix"] = [[n, 1.0 / len(names)] for n in names]
+        return dict(base, workload=w, h2d=h2d)
+    t90 = tmax
 
     # ---- warm-up: capacity search (largest offered rate with on-time >= 0.9)
     warm_runs = []
@@ -164,7 +199,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
         warm_runs.append((rate, r["on_time_ratio_f"]))
         return r["on_time_ratio_f"] >= 0.90
 
-    est = 90.0 / t90 * 1000.0  # full-batch throughput of the table
+    est = mb / t90 * 1000.0  # full-batch throughput of the table (slowest DNN)
     lo, hi = None, None
     rate = 0.5 * est
     while len(warm_runs) < 14:
@@ -252,7 +287,8 @@ def run_ours(a, ws, rank, local) -> dict | None:
     if rank != 0:
         return None
     out = {
-        "metric": METRIC,
+        "metric": METRIC if a.config == 2 else
+        f"served requests/s ({cfg['process']}, on-time >= 0.90 capacity point), config {a.config}",
         "value": round(tot_completed / (t_max / 1000.0), 2) if t_max else 0.0,
         "unit": UNIT,
         "n_gpus": ws,
@@ -266,15 +302,15 @@ def run_ours(a, ws, rank, local) -> dict | None:
         "data": "synthetic images (SplitMix64 N(0,1)), deterministic random-init weights",
         "on_time_ratio": round(tot_on / tot_gen, 4) if tot_gen else None,
         "config": {
-            "workload": "config 2: GoogLeNet 224x224 single DNN, Poisson arrivals, Our-Tardy (on-time objective), "
-                        "partial batching at layer granularity, B=90, 1 server per GPU",
+            "workload": cfg["workload"],
+            "suite": cfg["suite"],
             "offered_rate_per_gpu": round(cap, 1),
             "capacity_search_rate": round(cap_search, 1),
             "requests_per_step": a.requests,
             "deadline_ms": round(deadline, 4),
             "t1_ms": round(t1, 4),
-            "t90_ms": round(t90, 4),
-            "max_batch": 90,
+            "t_max_batch_ms": round(t90, 4),
+            "max_batch": mb,
             "precision": a.precision,
             "l2": "no flush: each step touches R x 4.6 MB request blobs (>> 126 MB L2) plus 26 MB of weights",
             "parallelism": f"{ws} independent servers (request streams sharded, no collectives)",
@@ -323,8 +359,8 @@ def cpu_baseline(ex, a) -> dict:
         orc.forward(img)
     dt = time.perf_counter() - t
     return {"value": round(len(imgs) / dt, 3), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{len(imgs)} GoogLeNet requests through all 22 layers with the builder's numpy fp32 "
-                      f"oracle (BLAS on all host threads); the reference batchsim executes no layers",
+            "sample": f"{len(imgs)} {n['name']} requests through all {len(n['layers'])} layers with the builder's "
+                      f"numpy fp32 oracle (BLAS on all host threads); the reference batchsim executes no layers",
             "seconds": round(dt, 2)}
 
 
@@ -392,7 +428,9 @@ def main() -> None:
     ap.add_argument("--precision", default="tf32x2", choices=["tf32x2", "tf32"])
     ap.add_argument("--stats-every", type=int, default=4)
     ap.add_argument("--cpu-requests", type=int, default=4)
-    ap.add_argument("--deadline-ms", type=float, default=5.0)
+    ap.add_argument("--deadline-ms", type=float, default=5.0, help="config 2 target (fixed)")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE.json config to serve (2 = the headline line)")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     ws, rank, local = dist_init()

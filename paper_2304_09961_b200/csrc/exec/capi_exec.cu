@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // C-ABI of libbs_exec.so (declared in include/bs_exec.h).
 #include <chrono>
 #include <cstdlib>
@@ -91,8 +93,10 @@ struct ReplayHook : batchsim::StepHook {
   int max_batch_seen = 0;
   long steps = 0;
 
-  void admit(batchsim::RequestId id, int dnn, int entry_layer, batchsim::Ms) override {
+  bool log = std::getenv("BS_REPLAY_LOG") != nullptr;
+  void admit(batchsim::RequestId id, int dnn, int entry_layer, batchsim::Ms t) override {
     const int net = dnn_map[static_cast<std::size_t>(dnn)];
+    if (log) std::fprintf(stderr, "t=%.3f admit %lld net %d entry %d\n", t, static_cast<long long>(id), net, entry_layer);
     const NetDef& nd = ex->suite().nets[static_cast<std::size_t>(net)];
     if (pool && ex->pool_size(net) > 0) {
       ex->admit(id, net, entry_layer, ex->pool_image(net, static_cast<int>((id - 1) % ex->pool_size(net))), true);
@@ -105,6 +109,12 @@ struct ReplayHook : batchsim::StepHook {
   }
   void plan(int plan_no, batchsim::Ms) override { ex->new_plan(plan_no); }
   void step(const batchsim::StepView& v) override {
+    if (log) {
+      std::fprintf(stderr, "t=%.3f step plan %d seg %d net %d [%d,%d]:", v.start, v.plan, v.segment,
+                   dnn_map[static_cast<std::size_t>(v.dnn)], v.from, v.to);
+      for (const auto& [id, layer] : v.members) std::fprintf(stderr, " %lld@%d", static_cast<long long>(id), layer);
+      std::fprintf(stderr, "\n");
+    }
     ex->step(v.plan, v.segment, dnn_map[static_cast<std::size_t>(v.dnn)], v.from, v.to, v.members, v.riders);
     max_batch_seen = std::max(max_batch_seen, static_cast<int>(v.members.size() + v.riders.size()));
     ++steps;

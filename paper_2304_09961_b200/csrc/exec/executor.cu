@@ -52,6 +52,12 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   total_slots_ = static_cast<long>(n_slots_) + n_ride_ + max_batch_;
   ck(cudaMalloc(&arena_, static_cast<std::size_t>(total_slots_) * slot_floats_ * sizeof(float)), "arena");
   for (int i = n_slots_ - 1; i >= 0; --i) free_.push_back(i);
+  // A freed slot may still be read by work queued on the serving stream (the
+  // retiring request's D2H copy of its probabilities); its next admission
+  // writes it from the copy or side stream, so it first waits on this event.
+  slot_free_ev_.resize(static_cast<std::size_t>(n_slots_));
+  slot_free_pending_.assign(static_cast<std::size_t>(n_slots_), 0);
+  for (auto& e : slot_free_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "slot event");
   ride_arena_ = arena_ + static_cast<std::size_t>(n_slots_) * slot_floats_;
   for (int i = n_ride_ - 1; i >= 0; --i) ride_free_.push_back(i);
   int max_layers = 1;
@@ -167,6 +173,7 @@ Executor::~Executor() {
   }
   if (copy_) cudaStreamSynchronize(copy_);
   for (cudaEvent_t e : ready_ring_) cudaEventDestroy(e);
+  for (cudaEvent_t e : slot_free_ev_) cudaEventDestroy(e);
   cudaFree(staging_);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (float* p : pool_) cudaFree(p);
@@ -330,6 +337,7 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
   const TensorDef& in = net.tensors[static_cast<std::size_t>(net.input_t)];
   const std::size_t bytes = static_cast<std::size_t>(in.H) * in.W * in.C * sizeof(float);
   cudaStream_t st = entry_layer > 1 ? side_ : copy_;
+  wait_slot_free(s.index, st);
   ck(cudaMemcpyAsync(s.blob + in.off, image, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
      "admit copy");
   if (entry_layer == 1) {
@@ -385,11 +393,19 @@ void Executor::admit_rgb(std::int64_t id, int dnn, const float* rgb) {
   staging_next_ = (staging_next_ + 1) % staging_n_;  // ring reuse is ordered on copy_
   ck(cudaMemcpyAsync(stage, rgb, static_cast<std::size_t>(hw) * 3 * sizeof(float), cudaMemcpyHostToDevice, copy_),
      "admit rgb H2D");
+  wait_slot_free(s.index, copy_);
   ck(launch_expand_rgb(stage, s.blob + in.off, hw, copy_), "expand rgb");
   s.ready = next_ready_event();
   ck(cudaEventRecord(s.ready, copy_), "ready rec");
   s.pending_ready = true;
   slot_of_.emplace(id, s);
+}
+
+void Executor::wait_slot_free(int index, cudaStream_t st) {
+  const std::size_t i = static_cast<std::size_t>(index);
+  if (!slot_free_pending_[i]) return;
+  ck(cudaStreamWaitEvent(st, slot_free_ev_[i], 0), "wait slot free");
+  slot_free_pending_[i] = 0;
 }
 
 const float* Executor::blob(std::int64_t id) const {
@@ -419,7 +435,7 @@ void Executor::retire_async(std::int64_t id, float* out, int n) {
   ck(cudaMemcpyAsync(out, it->second.blob + t.off, static_cast<std::size_t>(cnt) * sizeof(float),
                      cudaMemcpyDeviceToHost, stream_),
      "retire copy");
-  drop(id);  // slot reuse is stream-ordered after the copy
+  drop(id);  // the slot's next admission waits for this copy (slot_free_ev_)
 }
 
 void Executor::drop(std::int64_t id) {
@@ -429,6 +445,9 @@ void Executor::drop(std::int64_t id) {
     // a pending input copy / prefix must finish before the slot can be reused
     ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
   }
+  const std::size_t idx = static_cast<std::size_t>(it->second.index);
+  ck(cudaEventRecord(slot_free_ev_[idx], stream_), "slot free rec");
+  slot_free_pending_[idx] = 1;
   free_.push_back(it->second.index);
   slot_of_.erase(it);
   auto r = ride_of_.find(id);
@@ -510,7 +529,16 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
   std::vector<LayerRun> runs;
   std::vector<std::pair<int, RideRun>> copies;  // (layer before which to copy, ride)
   std::size_t mi = 0;
-  for (int k = from; k <= to; ++k) {
+  // The reference DP sets a segment's start layer to its newest member's
+  // layer (dp_time.hpp:279), assuming FIFO order implies non-increasing
+  // layers. With collaborative admission an older request can arrive later
+  // at a lower layer; the simulator then advances it to layer_to + 1
+  // (simulator.hpp:475-516) although layers [its layer, from) never ran.
+  // Schedules stay bit-exact; the executor runs those layers for such members
+  // inside this step, so outputs remain the network's.
+  int first = from;
+  for (const auto& m : mem) first = std::min(first, m.first);
+  for (int k = first; k <= to; ++k) {
     while (mi < mem.size() && mem[mi].first <= k) ++mi;
     int nr = 0;
     for (const RideRun& rr : rides)

@@ -130,6 +130,9 @@ class Executor {
   std::size_t slot_floats_ = 0;
   int n_slots_ = 0;
   std::vector<int> free_;
+  std::vector<cudaEvent_t> slot_free_ev_;  // recorded on stream_ when a slot is freed
+  std::vector<char> slot_free_pending_;
+  void wait_slot_free(int index, cudaStream_t st);
   std::unordered_map<std::int64_t, Slot> slot_of_;
   // ride buffers: rider id -> ride slot index (valid for the current plan)
   float* ride_arena_ = nullptr;

@@ -222,6 +222,8 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
     const int per = (KT + ks - 1) / ks;
     ks = (KT + per - 1) / per;
   }
+  static const int dbg = std::getenv("BS_CONV_DEBUG") ? std::atoi(std::getenv("BS_CONV_DEBUG")) : 0;
+  p.debug = dbg;
   p.ksplits = std::max(1, ks);
   p.kt_per_split = (KT + p.ksplits - 1) / p.ksplits;
   p.partials = ws.partials;

@@ -93,6 +93,7 @@ struct ConvParams {
   int Win, Hin, ktpc;
   int win_img_bytes;            // smem stride between the G image windows (1024-aligned)
   int win_tx_bytes;             // bytes one image window box delivers
+  int debug;                    // experiment switches (0 in production; BS_CONV_DEBUG)
 };
 
 // Device workspace for split-K (owned by the caller; counters zeroed once).
@@ -439,9 +440,11 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
         if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t dst = lane_base + sa * S::kACols;
-        ptx::tmem_st32(dst, hi);
-        if constexpr (SPLIT) ptx::tmem_st32(dst + kBK, lo);
-        ptx::tmem_st_wait();
+        if (!(p.debug & 1)) {
+          ptx::tmem_st32(dst, hi);
+          if constexpr (SPLIT) ptx::tmem_st32(dst + kBK, lo);
+          ptx::tmem_st_wait();
+        }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&ta_full[sa]);
         if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 3] = gtime();
@@ -667,7 +670,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
                 __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(out_row), rl);
             const unsigned long long rp =
                 __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(res_row), rl);
-            if (!op || !col_ok) continue;
+            if (!op || !col_ok || (p.debug & 4)) continue;
             float4 x = ptx::lds128(stage + rl * 128 + ((cq ^ (rl & 7)) << 4));
             float* dst = reinterpret_cast<float*>(op) + nc;
             const float* rr = reinterpret_cast<const float*>(rp);
@@ -788,7 +791,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           for (int k = 0; k < kBK / 8; ++k) {
             // A: 8 TMEM columns per K=8 step; B: +32 bytes inside the swizzled row.
             ptx::mma_tf32_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
-            if constexpr (SPLIT) ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
+            if constexpr (SPLIT)
+              if (!(p.debug & 2)) ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
           }
           ptx::mma_commit(&ta_empty[sa]);  // == b_empty[sb]
           if (kt == w.kt1 - 1) ptx::mma_commit(&acc_full[acc]);

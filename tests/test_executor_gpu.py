@@ -181,3 +181,81 @@ def test_live_serve_small():
         r = ex.serve(job)
         assert r["completed"] + r["dropped"] == 300
         assert r["completed"] > 0 and r["launches"] > 0
+
+
+def _check_replay_outputs(ex, out, image_seed, orcs, per_dnn=3):
+    """Every request served on the B200 (up to per_dnn per DNN) against the
+    CPU oracle of its own DNN."""
+    outcomes = next(r for r in out if r["ev"] == "outcomes")["outcomes"]
+    res = next(r for r in out if r["ev"] == "results")
+    seen = {}
+    checked = 0
+    for o in outcomes:
+        rid, dnn, location = o[0], o[1], o[7]
+        if location == 1 or o[6]:  # finished on the client / dropped: no server output
+            continue
+        if seen.get(dnn, 0) >= per_dnn or str(rid) not in res["probs"]:
+            continue
+        seen[dnn] = seen.get(dnn, 0) + 1
+        orc = orcs[dnn]
+        ref = orc.probs(orc.forward(image_for(ex, dnn, rid - 1, seed=image_seed)))
+        got = np.array(res["probs"][str(rid)], np.float32)[:ref.size]
+        assert rel_err(got, ref) < TOL, (rid, dnn)
+        assert int(np.argmax(got)) == int(np.argmax(ref)) == res["top1"][rid - 1]
+        checked += 1
+    return seen, checked
+
+
+def test_hetero3_replay_config4():
+    """Config 4: GoogLeNet + ResNet-50 + MobileNetV2 (no shared layers),
+    equal Poisson mix, multi-DNN permutation DP; every step runs on the
+    GPU and sampled requests of each DNN match the oracle."""
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("hetero3", max_batch=90, max_requests=64) as ex:
+        w = ex.weights()
+        orcs = [NetOracle(ex.desc, k, w) for k in range(3)]
+        names = [n["name"] for n in ex.desc["nets"]]
+        job = {"profile": synth_profile(ex, 1.0, 0.02),
+               "workload": {"process": "poisson", "rate": 600, "count": 30, "seed": 3,
+                            "dnn_mix": [[n, 1.0 / 3] for n in names]},
+               "sim": {"scheduler": "ours-time", "granularity": "group", "max_batch": 90},
+               "image_seed": 5, "dump_ids": list(range(1, 31))}
+        out = ex.replay(job)
+        summ = next(r for r in out if r["ev"] == "summary")
+        res = next(r for r in out if r["ev"] == "results")
+        assert summ["completed"] == 30
+        assert res["max_step_batch"] > 1
+        seen, checked = _check_replay_outputs(ex, out, 5, orcs, per_dnn=2)
+        assert set(seen) == {0, 1, 2} and checked == 6
+
+
+def test_collab_partial_replay_config5():
+    """Config 5: collaborative partial offload (client prefix of k layer
+    groups, server suffix from the entry layer), Pareto arrivals, the LTE
+    trace x10 and the Jetson client profile; requests admitted at
+    entry_layer > 1 finish on the GPU with the full network's outputs."""
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("collab", max_batch=90, max_requests=64) as ex:
+        w = ex.weights()
+        orcs = [NetOracle(ex.desc, k, w) for k in range(2)]
+        names = [n["name"] for n in ex.desc["nets"]]
+        job = {"profile": synth_profile(ex, 1.0, 0.02),
+               "workload": {"process": "pareto", "rate": 60, "count": 24, "seed": 11,
+                            "dnn_mix": [[n, 0.5] for n in names]},
+               "sim": {"scheduler": "ours-time", "granularity": "group", "max_batch": 90,
+                       "offload": "partial", "clients": 4},
+               "client_profile": "tests/golden/ref_data/jetson_nano.json",
+               "trace": "tests/golden/ref_data/lte_uplink.csv", "trace_scale": 10.0,
+               "image_seed": 9, "dump_ids": list(range(1, 25))}
+        import os
+        cwd = os.getcwd()
+        os.chdir(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        try:
+            out = ex.replay(job)
+        finally:
+            os.chdir(cwd)
+        outcomes = next(r for r in out if r["ev"] == "outcomes")["outcomes"]
+        partial = [o for o in outcomes if o[7] == 2]  # client_partial: prefix on the client
+        assert partial, "no request was split between client and server"
+        seen, checked = _check_replay_outputs(ex, out, 9, orcs, per_dnn=3)
+        assert checked >= 3
