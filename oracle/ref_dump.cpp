@@ -451,6 +451,26 @@ int main(int argc, char** argv) {
     std::ostringstream out;
     if (kind == "sim") {
       run_sim_job(job, out);
+    } else if (kind == "report") {
+      // The reference's own result writers (report.hpp:35-65) on run_sim:
+      // outcome CSV, then a "--" line, then summary_json(...).dump(1).
+      SimJob sj = sim_job_from(job);
+      const SimResult res = run_sim(sj.spec, sj.ps, sj.config, sj.trace ? &*sj.trace : nullptr,
+                                    sj.client ? &*sj.client : nullptr);
+      write_outcomes_csv(out, res.outcomes, sj.ps);
+      out << "--\n" << summary_json(res.metrics).dump(1) << '\n';
+    } else if (kind == "sweep") {
+      // capacity_sweep (simulator.hpp:806-820): per rate the on-time ratio and
+      // mean completion (seconds) as IEEE bit patterns.
+      SimJob sj = sim_job_from(job);
+      const std::vector<double> rates = job.at("rates").get<std::vector<double>>();
+      const auto curve = capacity_sweep(sj.spec, rates, sj.ps, sj.config, sj.trace ? &*sj.trace : nullptr,
+                                        sj.client ? &*sj.client : nullptr);
+      for (std::size_t r = 0; r < rates.size(); ++r)
+        out << json{{"rate", rates[r]}, {"ratio", bits(curve.points[r].metrics.on_time_ratio)},
+                    {"mean_completion_s", bits(curve.points[r].metrics.mean_completion / 1000.0)}}
+                   .dump()
+            << '\n';
     } else if (kind == "random") {
       run_random_job(job, out);
     } else if (kind == "calls") {

@@ -2,6 +2,7 @@
 
   lib/libbs_host.so  C++20 host scheduler + event loop (no CUDA)
   lib/libbs_exec.so  sm_100a kernels + executor + arena + C-ABI (links host objects)
+  bin/batchsim_b200  CLI: simulate / sweep-capacity / validate-profile / oracle-check
 
 Both are built with -ffp-contract=off so host double arithmetic matches the
 reference's.
@@ -19,6 +20,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "lib"
+BIN = PKG / "bin"
 OBJ = ROOT / "build" / "obj"
 INCLUDE = ROOT / "include"
 # nlohmann/json (header-only parser; the copy shipped in this image's
@@ -100,6 +102,14 @@ def build(verbose: bool = False) -> dict[str, Path]:
     if host_objs:
         _run(["g++", "-shared", "-o", str(host_so), *map(str, host_objs)])
         out["host"] = host_so
+    # Native CLI with the reference's subcommands (csrc/cli), linked against
+    # the host objects only (no CUDA).
+    cli_objs = [_compile(s, digest) for s in _sources("cli", (".cpp",))]
+    if cli_objs:
+        BIN.mkdir(parents=True, exist_ok=True)
+        cli = BIN / "batchsim_b200"
+        _run(["g++", "-o", str(cli), *map(str, cli_objs), *map(str, host_objs)])
+        out["cli"] = cli
     exec_so = LIB / "libbs_exec.so"
     _run([NVCC, "-shared", *GENCODE, "-o", str(exec_so), *map(str, exec_objs),
           *map(str, host_objs), "-lcudart"])
