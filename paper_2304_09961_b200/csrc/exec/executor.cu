@@ -89,14 +89,19 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   }
   // One TMA descriptor per conv/FC weight matrix (weights never move).
   wmaps_.resize(suite_.nets.size());
+  wmaps_wide_.resize(suite_.nets.size());
   for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
     const NetDef& net = suite_.nets[n];
     wmaps_[n].resize(net.ops.size());
+    wmaps_wide_[n].resize(net.ops.size());
     for (std::size_t i = 0; i < net.ops.size(); ++i) {
       const OpDef& op = net.ops[i];
       if (op.kind != OpKind::conv) continue;
       if (!encode_weight_map(&wmaps_[n][i], d_weights_ + op.w_off, op.out.C, op.Kpad))
         throw std::runtime_error("cuTensorMapEncodeTiled failed for " + op.name);
+      if (op.out.C > 128 &&
+          !encode_weight_map(&wmaps_wide_[n][i], d_weights_ + op.w_off, op.out.C, op.Kpad, 256))
+        throw std::runtime_error("cuTensorMapEncodeTiled (wide) failed for " + op.name);
     }
   }
   // Window mode for spatial convs (opt-in, BS_CONV_WIN=1; measured slower
@@ -244,6 +249,9 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
     case OpKind::conv: {
       ConvParams p{};
       p.wmap = wmaps_[static_cast<std::size_t>(&net - suite_.nets.data())][static_cast<std::size_t>(&op - net.ops.data())];
+      if (op.out.C > 128)
+        conv_add_wide_map(p, wmaps_wide_[static_cast<std::size_t>(&net - suite_.nets.data())]
+                                        [static_cast<std::size_t>(&op - net.ops.data())]);
       p.nimg = batch;
       p.H = ti.H;
       p.W = ti.W;

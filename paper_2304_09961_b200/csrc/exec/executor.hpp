@@ -160,6 +160,7 @@ class Executor {
   std::vector<float*> pool_;
   std::vector<int> pool_n_;
   std::vector<std::vector<CUtensorMap>> wmaps_;  // [net][op] weight tensor maps
+  std::vector<std::vector<CUtensorMap>> wmaps_wide_;  // [net][op] 256-row boxes (N > 128)
   struct ActMap {
     CUtensorMap map{};
     ActGeom geom;

@@ -72,6 +72,14 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
       rc = bs_fail(BS_ECUDA, "cuTensorMapEncodeTiled failed");
       goto done;
     }
+    if (d->N > 128) {
+      CUtensorMap wide;
+      if (!encode_weight_map(&wide, dw, d->N, Kpad, 256)) {
+        rc = bs_fail(BS_ECUDA, "cuTensorMapEncodeTiled (wide) failed");
+        goto done;
+      }
+      conv_add_wide_map(p, wide);
+    }
     p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_off = d->out_coff;
     p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_off = d->res_coff;
     p.relu = d->relu; p.round_out = d->round_out; p.split = d->split;

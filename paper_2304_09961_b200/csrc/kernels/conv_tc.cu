@@ -36,6 +36,28 @@ cudaError_t launch_bn(const ConvParams& p, int grid, cudaStream_t stream) {
 
 int conv_tile_n(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : 128; }
 
+namespace {
+// 128 x 256 tiles for N > 128. The A path (gather + conversion) costs about
+// the same per K tile whatever the tile width, so the wide tile halves it per
+// FLOP, but it has a single TMEM accumulator (epilogue not overlapped) and
+// half the tiles. Measured on B200 (profiles/r01/layers_b90_bn*.csv): a wide
+// K tile costs ~1.8x a narrow one, so wide pays when it cuts the N tiles by
+// more than 1.8x, the K loop is long (K >= 512) and the tiles still fill the
+// GPU. BS_CONV_BN256=0 disables, =2 forces (when a wide weight map exists).
+bool use_wide(const ConvParams& p, int sms) {
+  const char* env = std::getenv("BS_CONV_BN256");  // read per launch (tests toggle it)
+  if (!p.has_wide || p.a_win || (env && env[0] == '0')) return false;
+  if (env && env[0] == '2') return true;
+  const int narrow = (p.N + 127) / 128, wide = (p.N + 255) / 256;
+  return p.N > 128 && p.K >= 512 && wide * 1.8 < narrow && p.m_tiles * wide * 10 >= sms * 9;
+}
+}  // namespace
+
+void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide) {
+  p.wmap_wide = wide;
+  p.has_wide = 1;
+}
+
 std::size_t conv_workspace_floats() { return static_cast<std::size_t>(2 * 160) * conv_tc::kBM * 128; }
 int conv_workspace_counters() { return 2 * 2 * 160; }
 
@@ -58,12 +80,13 @@ EncodeTiledFn encode_fn() {
 }
 }  // namespace
 
-bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad) {
+bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad, int box_n) {
   const EncodeTiledFn encode = encode_fn();
   if (!encode) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kpad), static_cast<cuuint64_t>(N)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kpad) * sizeof(float)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(conv_tc::kBK), static_cast<cuuint32_t>(conv_tile_n(N))};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(conv_tc::kBK),
+                             static_cast<cuuint32_t>(box_n > 0 ? box_n : conv_tile_n(N))};
   const cuuint32_t elem[2] = {1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(w), dims, strides, box,
                                 elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -185,16 +208,20 @@ void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& g, c
 cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t stream) {
   if (p.Cin % 4 != 0 || p.Kpad % conv_tc::kBK != 0 || p.Kpad < p.K || p.nimg <= 0)
     return cudaErrorInvalidValue;
-  const int bn = conv_tile_n(p.N);
+  int bn = conv_tile_n(p.N);
   const int sms = sm_count();
   const int KT = p.Kpad / conv_tc::kBK;
   if (p.a_tma && (p.G < 1 || p.G > 4 || p.Wb * p.Hb * p.G != conv_tc::kBM || p.a_g % 4 || p.Cin % p.a_g))
     return cudaErrorInvalidValue;
-  if (p.a_win && (!p.a_tma || p.G * p.win_img_bytes > conv_tc::kWinBytes || p.ktpc <= 0 ||
+  if (p.a_win && (!p.a_tma || bn > 128 || p.G * p.win_img_bytes > conv_tc::kWinBytes || p.ktpc <= 0 ||
                   p.Kpad != (p.Cin / p.a_g) * p.ktpc * conv_tc::kBK))
     return cudaErrorInvalidValue;
   p.m_tiles = p.a_tma ? (p.G == 1 ? p.nimg * p.tpi : (p.nimg + p.G - 1) / p.G)
                       : (p.nimg * p.Ho * p.Wo + conv_tc::kBM - 1) / conv_tc::kBM;
+  if (use_wide(p, sms)) {
+    bn = 256;
+    p.wmap = p.wmap_wide;
+  }
   p.n_tiles = (p.N + bn - 1) / bn;
   const int tiles = p.m_tiles * p.n_tiles;
   // Split K when the tiles cannot cover the SMs (small merged batches).
@@ -237,11 +264,13 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   if (p.split) {
     if (bn == 32) return launch_bn<32, true>(p, grid, stream);
     if (bn == 64) return launch_bn<64, true>(p, grid, stream);
-    return launch_bn<128, true>(p, grid, stream);
+    if (bn == 128) return launch_bn<128, true>(p, grid, stream);
+    return launch_bn<256, true>(p, grid, stream);
   }
   if (bn == 32) return launch_bn<32, false>(p, grid, stream);
   if (bn == 64) return launch_bn<64, false>(p, grid, stream);
-  return launch_bn<128, false>(p, grid, stream);
+  if (bn == 128) return launch_bn<128, false>(p, grid, stream);
+  return launch_bn<256, false>(p, grid, stream);
 }
 
 }  // namespace bs200

@@ -94,6 +94,8 @@ struct ConvParams {
   int win_img_bytes;            // smem stride between the G image windows (1024-aligned)
   int win_tx_bytes;             // bytes one image window box delivers
   int debug;                    // experiment switches (0 in production; BS_CONV_DEBUG)
+  CUtensorMap wmap_wide;        // weights with a 256-row box (N > 128), used for 128 x 256 tiles
+  int has_wide;
 };
 
 // Device workspace for split-K (owned by the caller; counters zeroed once).
@@ -121,9 +123,12 @@ constexpr int kWinBytes = 65536;  // one input window (window mode); two share t
 template <int BN, bool SPLIT>
 struct Cfg {
   static constexpr int kThreads = 608;
-  static constexpr int RA = BN == 32 ? 10 : 8;
+  // BN = 256: one accumulator (256 columns) so the A slots still fit in TMEM;
+  // the raw A ring shrinks to make room for the 32 KB B stages.
+  static constexpr int kAcc = BN == 256 ? 1 : 2;                 // TMEM accumulator buffers
+  static constexpr int RA = BN == 32 ? 10 : BN == 256 ? 6 : 8;
   static constexpr int kACols = SPLIT ? 2 * kBK : kBK;          // TMEM columns per A slot
-  static constexpr int kTA0 = 2 * BN;                            // first A column (after 2 accumulators)
+  static constexpr int kTA0 = kAcc * BN;                         // first A column (after the accumulators)
   // One operand stage = (TMEM A slot, B smem stage), released by a single
   // tcgen05.commit per K tile (each commit costs the tensor pipe ~84 cycles).
   static constexpr int kTAmax = (512 - kTA0) / kACols;
@@ -138,7 +143,7 @@ struct Cfg {
   static constexpr int kTotal = kBarOffset + 512 + 1024;        // barriers + alignment slack
   static_assert(kTotal <= 232448, "shared memory budget");
   static_assert(TA >= 2, "TMEM budget");
-  static_assert(RA * kABytes >= 2 * kWinBytes, "window ring");
+  static_assert(BN == 256 || RA * kABytes >= 2 * kWinBytes, "window ring");
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -625,8 +630,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = unit_of(p, u, BN, KT);
-      const int acc = j & 1;
-      ptx::mbar_wait(&acc_full[acc], (j >> 1) & 1);
+      const int acc = j % S::kAcc;
+      ptx::mbar_wait(&acc_full[acc], (j / S::kAcc) & 1);
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       int n_img = 0, pix = 0;
@@ -646,7 +651,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           ptx::tmem_ld_wait();
           if (jj == BN / 32 - 1) {
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&acc_empty[acc]);  // TMEM buffer free for unit j + 2
+            ptx::mbar_arrive(&acc_empty[acc]);  // TMEM buffer free for unit j + kAcc
           }
           const int n0 = w.n_base + jj * 32;
           if (n0 >= p.N) continue;  // warp-uniform
@@ -774,8 +779,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     int it = 0, j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = unit_of(p, u, BN, KT);
-      const int acc = j & 1;
-      if (j >= 2) ptx::mbar_wait(&acc_empty[acc], ((j >> 1) - 1) & 1);
+      const int acc = j % S::kAcc;
+      if (j >= S::kAcc) ptx::mbar_wait(&acc_empty[acc], ((j / S::kAcc) - 1) & 1);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
@@ -834,7 +839,8 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
 
 }  // namespace conv_tc
 
-// N tile the launcher uses for N output channels.
+// Narrow N tile for N output channels (the launcher may widen to 256, see
+// conv_add_wide_map).
 int conv_tile_n(int N);
 
 // Box geometry of the TMA activation path for a conv with Cin (padded)
@@ -874,7 +880,9 @@ void conv_use_window(ConvParams& p, const CUtensorMap& amap, const CUtensorMap& 
 void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& geom, const float* slot_base,
                       long slot_floats, long slots);
 // Encodes a weight tensor map for w ([N][Kpad] floats) and the tile conv_tile_n(N).
-bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad);
+bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad, int box_n = 0);
+// Offers the launcher 128 x 256 tiles (weights map with box_n = 256).
+void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide);
 // Host-side launcher: chooses the K split, grid and workspace use
 // (p.wmap must be encoded for conv_tile_n(p.N)).
 cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t stream);

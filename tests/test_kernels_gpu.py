@@ -144,3 +144,14 @@ def test_conv_tma_activation_path(case, monkeypatch):
     """TMA activation boxes (BS_CONV_TMA=1) on the same layers as the cp.async gather."""
     monkeypatch.setenv("BS_CONV_TMA", "1")
     assert run_conv(**case) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [c for c in CASES if c["N"] > 128] + [
+    dict(nimg=9, H=14, W=14, Cin=64, N=208, KH=3, KW=3, stride=1, pad=1)],
+    ids=lambda c: "x".join(str(c[k]) for k in ("nimg", "H", "Cin", "N", "KH", "stride")))
+@pytest.mark.parametrize("split", [1, 0])
+def test_conv_wide_tiles(case, split, monkeypatch):
+    """128 x 256 tiles (single TMEM accumulator), forced with BS_CONV_BN256=2."""
+    monkeypatch.setenv("BS_CONV_BN256", "2")
+    assert run_conv(**case, split=split) < TOL
