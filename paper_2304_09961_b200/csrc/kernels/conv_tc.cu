@@ -230,15 +230,20 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   // with every unit of a split-K launch co-resident (units <= SMs) so the
   // cooperative reduction can wait on its tile's splits.
   int ks = 1;
+  // Split-K cost model: a split unit pays the partial-tile round trip and the
+  // cross-CTA wait, worth ~24 K tiles of work (fitted on the GoogLeNet
+  // latency table, b = 1..64; knobs BS_CONV_KS_MAX / BS_CONV_KS_OVH).
+  static const int ks_max = std::getenv("BS_CONV_KS_MAX") ? std::atoi(std::getenv("BS_CONV_KS_MAX")) : 16;
+  static const int ks_ovh = std::getenv("BS_CONV_KS_OVH") ? std::atoi(std::getenv("BS_CONV_KS_OVH")) : 24;
   if (tiles < sms && ws.partials && ws.counters && 2 * tiles <= ws.n_counters) {
     auto cost = [&](int k) {
       const int per = (KT + k - 1) / k;
       const int units = tiles * k;
       const int waves = (units + sms - 1) / sms;
-      return waves * (per + (k > 1 ? 6 : 3));
+      return waves * (per + (k > 1 ? ks_ovh : 3));
     };
     int best = cost(1);
-    for (int k = 2; k <= 16 && tiles * k <= sms && k <= KT; ++k) {
+    for (int k = 2; k <= ks_max && tiles * k <= sms && k <= KT; ++k) {
       if (static_cast<std::size_t>(tiles) * k * conv_tc::kBM * bn > ws.partial_floats) break;
       const int c = cost(k);
       if (c < best) {
