@@ -222,24 +222,34 @@ def run_ours(a, ws, rank, local) -> dict | None:
     # near saturation and single runs vary by a few percent.
     cap = allreduce_max(-cap_search, ws) * -0.97  # same offered rate on every rank
 
-    # ---- timed steps at the capacity rate
-    ex.stats(True, every=a.stats_every)
-    completed = generated = on_time = launches = 0
-    device_ms = 0.0
-    sched = []
-    with ClockSampler(local) as clk:
-        barrier(ws)
-        t_wall = time.perf_counter()
-        for k in range(a.steps):
-            r = ex.serve(job(cap, a.requests, 5000 + k + 97 * rank))
-            completed += r["completed"]
-            generated += r["generated"]
-            on_time += r["on_time"]
-            launches += r["launches"]
-            device_ms += r["device_ms"]
-            sched.append(r)
-        barrier(ws)
-        wall_ms = (time.perf_counter() - t_wall) * 1000
+    # ---- timed steps at the capacity rate. The timed region must itself meet
+    # the 0.90 on-time bar (the capacity definition); if it does not, the
+    # rate is lowered by 4% and the K steps are timed again (at most twice).
+    retimed = []
+    for attempt in range(3):
+        ex.stats(True, every=a.stats_every)
+        completed = generated = on_time = launches = 0
+        device_ms = 0.0
+        sched = []
+        with ClockSampler(local) as clk:
+            barrier(ws)
+            t_wall = time.perf_counter()
+            for k in range(a.steps):
+                r = ex.serve(job(cap, a.requests, 5000 + k + 97 * rank))
+                completed += r["completed"]
+                generated += r["generated"]
+                on_time += r["on_time"]
+                launches += r["launches"]
+                device_ms += r["device_ms"]
+                sched.append(r)
+            barrier(ws)
+            wall_ms = (time.perf_counter() - t_wall) * 1000
+        ratio = allreduce_sum(on_time, ws) / max(1.0, allreduce_sum(generated, ws))
+        if ratio >= 0.90 or attempt == 2:
+            break
+        retimed.append([round(cap, 1), round(ratio, 4)])
+        ex.stats(False)
+        cap *= 0.96
     clocks = clk.summary()
     stats = ex.stats_summary(pk["hbm_gbs"], pk["tf32_tflops"])
     ex.stats(False)
@@ -316,6 +326,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "parallelism": f"{ws} independent servers (request streams sharded, no collectives)",
         },
         "capacity_search": [[round(r, 1), round(x, 4)] for r, x in warm_runs],
+        "retimed_below_target": retimed,
         "latency_ms": {"mean": round(statistics.mean(s["mean_completion_ms"] for s in sched), 4),
                        "p95": round(max(s["p95_completion_ms"] for s in sched), 4)},
         "scheduler_ms": {"mean_per_plan": round(sum(s["sched_ms_total"] for s in sched) /
@@ -423,7 +434,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--requests", type=int, default=3000, help="requests per timed step")
-    ap.add_argument("--warm-requests", type=int, default=1500)
+    ap.add_argument("--warm-requests", type=int, default=3000, help="requests per capacity-search run")
     ap.add_argument("--slots", type=int, default=4096, help="activation-arena slots")
     ap.add_argument("--precision", default="tf32x2", choices=["tf32x2", "tf32"])
     ap.add_argument("--stats-every", type=int, default=4)

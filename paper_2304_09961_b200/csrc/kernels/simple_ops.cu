@@ -1,4 +1,5 @@
 #include <cfloat>
+#include <cstdlib>
 
 #include "ptx.cuh"
 #include "simple_ops.cuh"
@@ -74,6 +75,63 @@ __global__ void __launch_bounds__(256) maxpool_unrolled_kernel(const PoolParams 
 #pragma unroll
     for (int j = 1; j < K * K; ++j) m = max4(m, v[j]);
     *reinterpret_cast<float4*>(p.out_ptrs[n] + p.out_off + (ho * p.Wo + wo) * p.out_ldc + c4 * 4) = m;
+  }
+}
+
+// 3x3 max-pool, 2x2 output block per thread (one channel quad): the
+// (S + 3)^2 input window is walked row by row and folded into the four
+// running maxima, so a stride-1 pool loads 16 inputs per 4 outputs (9 each
+// in the one-output form) and stride 2 loads 25 per 4. Consecutive threads
+// take consecutive channel quads (coalesced 16-byte accesses).
+template <int S>
+__global__ void __launch_bounds__(256) maxpool3_block_kernel(const PoolParams p) {
+  constexpr int IN = S + 3;  // input rows / cols of a 2x2 output block (windows [0,3) and [S,S+3))
+  const int C4 = p.C >> 2;
+  const int Bw = (p.Wo + 1) >> 1, Bh = (p.Ho + 1) >> 1;
+  const int total = p.nimg * Bh * Bw * C4;
+  const float4 ninf = make_float4(-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c4 = i % C4;
+    int r = i / C4;
+    const int bw = r % Bw;
+    r /= Bw;
+    const int bh = r % Bh;
+    const int n = r / Bh;
+    const int oh0 = 2 * bh, ow0 = 2 * bw;
+    const int h0 = oh0 * S - p.pad, w0 = ow0 * S - p.pad;
+    const float* in = p.in_ptrs[n] + p.in_off + c4 * 4;
+    float4 m[2][2] = {{ninf, ninf}, {ninf, ninf}};
+#pragma unroll
+    for (int dy = 0; dy < IN; ++dy) {
+      const int h = h0 + dy;
+      const bool hok = h >= 0 && h < p.H;
+      float4 v[IN];
+#pragma unroll
+      for (int dx = 0; dx < IN; ++dx) {
+        const int w = w0 + dx;
+        v[dx] = (hok && w >= 0 && w < p.W) ? __ldg(reinterpret_cast<const float4*>(in + (h * p.W + w) * p.in_ldc))
+                                            : ninf;
+      }
+      // column maxima of the two output columns' windows (cols [0,3), [S, S+3))
+      const float4 c0 = max4(max4(v[0], v[1]), v[2]);
+      const float4 c1 = max4(max4(v[S], v[S + 1]), v[S + 2]);
+      if (dy < 3) {
+        m[0][0] = max4(m[0][0], c0);
+        m[0][1] = max4(m[0][1], c1);
+      }
+      if (dy >= S) {
+        m[1][0] = max4(m[1][0], c0);
+        m[1][1] = max4(m[1][1], c1);
+      }
+    }
+    float* out = p.out_ptrs[n] + p.out_off + c4 * 4;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int oh = oh0 + a, ow = ow0 + b;
+        if (oh < p.Ho && ow < p.Wo) *reinterpret_cast<float4*>(out + (oh * p.Wo + ow) * p.out_ldc) = m[a][b];
+      }
   }
 }
 
@@ -234,7 +292,11 @@ cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {
   const long outs = static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4);
   if (p.stride == 1 && rows >= 148L * 2048 * 2)
     maxpool_rows_kernel<<<grid_for(rows), kThreads, 0, s>>>(p);
-  else if (p.k == 3)
+  else if (p.k == 3 && (p.stride == 1 || p.stride == 2) && !std::getenv("BS_POOL_SIMPLE")) {
+    const long blocks = static_cast<long>(p.nimg) * ((p.Ho + 1) / 2) * ((p.Wo + 1) / 2) * (p.C / 4);
+    if (p.stride == 1) maxpool3_block_kernel<1><<<grid_for(blocks), kThreads, 0, s>>>(p);
+    else maxpool3_block_kernel<2><<<grid_for(blocks), kThreads, 0, s>>>(p);
+  } else if (p.k == 3)
     maxpool_unrolled_kernel<3><<<grid_for(outs), kThreads, 0, s>>>(p);
   else if (p.k == 2)
     maxpool_unrolled_kernel<2><<<grid_for(outs), kThreads, 0, s>>>(p);

@@ -118,7 +118,8 @@ def test_conv_plain_tf32_on_fp32_inputs_is_worse():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("k,stride,pad,ceil,H", [(3, 1, 1, True, 14), (3, 2, 0, True, 112), (3, 2, 1, False, 56),
-                                                (2, 2, 0, True, 14), (3, 2, 0, True, 28), (3, 2, 0, True, 13)])
+                                                (2, 2, 0, True, 14), (3, 2, 0, True, 28), (3, 2, 0, True, 13),
+                                                (3, 1, 1, True, 7), (3, 2, 0, True, 15), (3, 1, 1, False, 9)])
 def test_maxpool_in_executor_layers(k, stride, pad, ceil, H):
     """Max-pool shapes of GoogLeNet/ResNet-50 through a one-op network
     (the executor's own launch path) against the oracle."""
