@@ -631,14 +631,17 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = unit_of(p, u, BN, KT);
       const int acc = j % S::kAcc;
-      ptx::mbar_wait(&acc_full[acc], (j / S::kAcc) & 1);
-      ptx::tc_fence_after();
-      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+      // Row pointers are global loads (the per-request blob table): issue
+      // them before waiting for the accumulator so their latency hides
+      // behind this unit's MMAs instead of serialising every epilogue.
       int n_img = 0, pix = 0;
       const bool m_ok = row_pixel(p, w.mt, row, n_img, pix);
       float* out_row = m_ok ? p.out_ptrs[n_img] + p.out_off + static_cast<long>(pix) * p.out_ldc : nullptr;
       const float* res_row =
           (m_ok && p.res_ptrs) ? p.res_ptrs[n_img] + p.res_off + static_cast<long>(pix) * p.res_ldc : nullptr;
+      ptx::mbar_wait(&acc_full[acc], (j / S::kAcc) & 1);
+      ptx::tc_fence_after();
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       if (p.ksplits == 1) {
         // Coalesced epilogue: each warp stages its 32 rows x 32 columns in
         // shared memory (16B chunks XOR-swizzled by row), then writes whole
