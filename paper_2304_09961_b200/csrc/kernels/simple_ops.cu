@@ -253,6 +253,77 @@ __global__ void dwconv_kernel(const DwParams p) {
   }
 }
 
+// Depthwise 3x3 (pad 1), 2x2 output block per thread and channel quad: the
+// (S + 3)^2 input window is loaded once (16 loads per 4 outputs at stride 1,
+// 25 at stride 2, against 36) and the nine weight quads once per block.
+template <int S>
+__global__ void __launch_bounds__(256) dwconv3_block_kernel(const DwParams p) {
+  constexpr int IN = S + 3;
+  const int C4 = p.C >> 2;
+  const int Bw = (p.Wo + 1) >> 1, Bh = (p.Ho + 1) >> 1;
+  const long total = static_cast<long>(p.nimg) * Bh * Bw * C4;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int c4 = static_cast<int>(i % C4);
+    long r = i / C4;
+    const int bw = static_cast<int>(r % Bw);
+    r /= Bw;
+    const int bh = static_cast<int>(r % Bh);
+    const int n = static_cast<int>(r / Bh);
+    const int oh0 = 2 * bh, ow0 = 2 * bw;
+    const int h0 = oh0 * S - 1, w0 = ow0 * S - 1;
+    const float* in = p.in_ptrs[n] + p.in_off + c4 * 4;
+    float4 k[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) k[t] = __ldg(reinterpret_cast<const float4*>(p.wgt + t * p.C + c4 * 4));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + c4 * 4));
+    float4 acc[2][2] = {{b, b}, {b, b}};
+#pragma unroll
+    for (int dy = 0; dy < IN; ++dy) {
+      const int h = h0 + dy;
+      const bool hok = h >= 0 && h < p.H;
+#pragma unroll
+      for (int dx = 0; dx < IN; ++dx) {
+        const int w = w0 + dx;
+        if (!(hok && w >= 0 && w < p.W)) continue;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(in + (static_cast<long>(h) * p.W + w) * p.in_ldc));
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int kh = dy - a * S, kw = dx - c * S;
+            if (kh < 0 || kh > 2 || kw < 0 || kw > 2) continue;  // compile-time after unrolling
+            const float4 kk = k[kh * 3 + kw];
+            acc[a][c].x = fmaf(v.x, kk.x, acc[a][c].x);
+            acc[a][c].y = fmaf(v.y, kk.y, acc[a][c].y);
+            acc[a][c].z = fmaf(v.z, kk.z, acc[a][c].z);
+            acc[a][c].w = fmaf(v.w, kk.w, acc[a][c].w);
+          }
+      }
+    }
+    float* out = p.out_ptrs[n] + p.out_off + c4 * 4;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int oh = oh0 + a, ow = ow0 + c;
+        if (oh >= p.Ho || ow >= p.Wo) continue;
+        float4 o = acc[a][c];
+        o.x = act(o.x, p.relu);
+        o.y = act(o.y, p.relu);
+        o.z = act(o.z, p.relu);
+        o.w = act(o.w, p.relu);
+        if (p.round_out) {
+          o.x = ptx::round_tf32(o.x);
+          o.y = ptx::round_tf32(o.y);
+          o.z = ptx::round_tf32(o.z);
+          o.w = ptx::round_tf32(o.w);
+        }
+        *reinterpret_cast<float4*>(out + (static_cast<long>(oh) * p.Wo + ow) * p.out_ldc) = o;
+      }
+  }
+}
+
 // One warp per image: max, sum of exp, normalise.
 __global__ void softmax_kernel(const SoftmaxParams p) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -313,7 +384,13 @@ cudaError_t launch_avgpool(const AvgPoolParams& p, cudaStream_t s) {
 
 cudaError_t launch_dwconv(const DwParams& p, cudaStream_t s) {
   if (p.C % 4) return cudaErrorInvalidValue;
-  dwconv_kernel<<<grid_for(static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4)), kThreads, 0, s>>>(p);
+  const long blocks = static_cast<long>(p.nimg) * ((p.Ho + 1) / 2) * ((p.Wo + 1) / 2) * (p.C / 4);
+  if (p.stride == 1 && !std::getenv("BS_DW_SIMPLE"))
+    dwconv3_block_kernel<1><<<grid_for(blocks), kThreads, 0, s>>>(p);
+  else if (p.stride == 2 && !std::getenv("BS_DW_SIMPLE"))
+    dwconv3_block_kernel<2><<<grid_for(blocks), kThreads, 0, s>>>(p);
+  else
+    dwconv_kernel<<<grid_for(static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4)), kThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
