@@ -748,23 +748,6 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
         float* part = p.partials + (static_cast<std::size_t>(u) * kBM + row) * BN;
 #pragma unroll 1
         for (int jj = 0; jj < BN / 32; ++jj) {
-          // Residual quads of this chunk (rows rq*4 + lane/8, 16-byte column
-          // chunk lane%8): all eight loads issued before the TMEM load so
-          // their latency overlaps it instead of serialising the store loop
-          // (measured: residual layers ran 3x slower than the same shape
-          // without a residual).
-          float4 rv[8];
-          if (p.res_ptrs) {
-            const int nc = w.n_base + jj * 32 + (lane & 7) * 4;
-#pragma unroll
-            for (int rq = 0; rq < 8; ++rq) {
-              const unsigned long long rp =
-                  __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(res_row), rq * 4 + (lane >> 3));
-              const float* rr = reinterpret_cast<const float*>(rp);
-              const bool ok = rr && nc + 3 < p.N && (reinterpret_cast<uintptr_t>(rr + nc) & 15) == 0;
-              rv[rq] = ok ? __ldg(reinterpret_cast<const float4*>(rr + nc)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-          }
           uint32_t v[32];
           ptx::tmem_ld32(tbase + jj * 32, v);
           ptx::tmem_ld_wait();
