@@ -115,18 +115,18 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     }
     unsigned long long* trace = nullptr;
     if (std::getenv("BS_CONV_TRACE")) {
-      CK(cudaMalloc(&trace, 8 * 2400));
-      CK(cudaMemset(trace, 0, 8 * 2400));
+      CK(cudaMalloc(&trace, 8 * 3600));
+      CK(cudaMemset(trace, 0, 8 * 3600));
       p.trace = trace;
       CK(launch_conv_tc(p, ws, 0));  // warm-up (TMEM/TMA descriptors, L2)
       CK(cudaDeviceSynchronize());
-      CK(cudaMemset(trace, 0, 8 * 2400));
+      CK(cudaMemset(trace, 0, 8 * 3600));
     }
     CK(launch_conv_tc(p, ws, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));
     if (trace) {
-      unsigned long long h[2400];
+      unsigned long long h[3600];
       CK(cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost));
       unsigned long long t0 = ~0ULL;
       for (int b = 0; b < 254; ++b)
@@ -141,6 +141,10 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
                      rel(h[1024 + it * 5]), rel(h[1025 + it * 5]), rel(h[1026 + it * 5]), rel(h[1027 + it * 5]),
                      rel(h[1028 + it * 5]), rel(h[2048 + it * 4]), rel(h[2049 + it * 4]), rel(h[2050 + it * 4]),
                      rel(h[2051 + it * 4]));
+      for (int j = 0; j < 32 && h[3072 + j * 8]; ++j)
+        std::fprintf(stderr, "  unit %2d epi wait %7lld acc_full %7lld chunks %7lld %7lld %7lld %7lld\n", j,
+                     rel(h[3072 + j * 8]), rel(h[3073 + j * 8]), rel(h[3074 + j * 8]), rel(h[3075 + j * 8]),
+                     rel(h[3076 + j * 8]), rel(h[3077 + j * 8]));
       p.trace = nullptr;
       cudaFree(trace);
     }

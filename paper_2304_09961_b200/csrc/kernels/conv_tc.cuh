@@ -133,14 +133,18 @@ struct Cfg {
   // One operand stage = (TMEM A slot, B smem stage), released by a single
   // tcgen05.commit per K tile (each commit costs the tensor pipe ~84 cycles).
   static constexpr int kTAmax = (512 - kTA0) / kACols;
-  static constexpr int kNBmax = (232448 - 1024 - 512 - RA * kBM * 128 - kBM * 32 * 4) / (BN * 128);
+  // Per epilogue warp: bias [2][BN] fp32, blob-table entries [2][32] (out,
+  // residual) and the unit's final row pointers [32] (out, residual).
+  static constexpr int kEpiWarpBytes = 8 * BN + 1536;
+  static constexpr int kNBmax = (232448 - 1024 - 512 - RA * kBM * 128 - kBM * 32 * 4 - 4 * kEpiWarpBytes) / (BN * 128);
   static constexpr int TA = kTAmax < kNBmax ? (kTAmax < 8 ? kTAmax : 8) : (kNBmax < 8 ? kNBmax : 8);
   static constexpr int NB = TA;
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kBOffset = RA * kABytes;
   static constexpr int kStagingOffset = kBOffset + NB * kBBytes;  // epilogue staging, 128 x 32 fp32
-  static constexpr int kBarOffset = kStagingOffset + kBM * 32 * 4;
+  static constexpr int kEpiOffset = kStagingOffset + kBM * 32 * 4;
+  static constexpr int kBarOffset = kEpiOffset + 4 * kEpiWarpBytes;
   static constexpr int kTotal = kBarOffset + 512 + 1024;        // barriers + alignment slack
   static_assert(kTotal <= 232448, "shared memory budget");
   static_assert(TA >= 2, "TMEM budget");
@@ -235,8 +239,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
   using S = Cfg<BN, SPLIT>;
   constexpr int RA = S::RA, NB = S::NB, TA = S::TA;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // Align by pointer arithmetic on the __shared__ array (not via uintptr_t)
+  // so accesses through `smem` stay LDS/STS instead of generic LD/ST.
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* ra_full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
   uint64_t* ra_empty = ra_full + RA;
   uint64_t* b_full = ra_empty + RA;
@@ -421,7 +426,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
         if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 2] = gtime();
         const uint32_t a_raw = smem_base + s * S::kABytes;
         float4 v[8];
-        if (!p.a_tma || p.a_g == kBK) {
+        if (p.debug & 16) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else if (!p.a_tma || p.a_g == kBK) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) v[c] = ptx::lds128(a_raw + roff[c]);
         } else {
@@ -628,20 +636,82 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     const int ew = warp - 4;
     const int row = ew * 32 + lane;
     const int et = threadIdx.x - 128;  // 0..127
+    // The epilogue's global loads (row base pointers from the per-request
+    // blob tables, the unit's bias slice) are issued one unit ahead: when the
+    // epilogue is the critical role (short-K layers) a load issued at the
+    // top of the unit sits behind the producers' traffic in L1 and stalls
+    // every chunk (measured ~1 us per chunk on 1x1 layers at b=90).
+    // They land by cp.async in this warp's double-buffered area, so they
+    // take no registers (held in registers they were spilled at once).
+    const uint32_t epi_s = smem_base + S::kEpiOffset + ew * S::kEpiWarpBytes;
+    uint8_t* epi_g = smem + S::kEpiOffset + ew * S::kEpiWarpBytes;
+    constexpr int kTabB = 8 * BN, kFinB = 8 * BN + 1024;
+    const unsigned long long* fin_out = reinterpret_cast<const unsigned long long*>(epi_g + kFinB);
+    const unsigned long long* fin_res = fin_out + 32;
+    auto prefetch = [&](int u, int buf) {
+      const Unit w = unit_of(p, u, BN, KT);
+      int n_img = 0, pix = 0;
+      const bool m_ok = row_pixel(p, w.mt, row, n_img, pix);
+      const int ic = m_ok ? n_img : 0;
+      ptx::cp_async8(epi_s + kTabB + (buf * 32 + lane) * 8, p.out_ptrs + ic, m_ok ? 8u : 0u);
+      if (p.res_ptrs) ptx::cp_async8(epi_s + kTabB + 512 + (buf * 32 + lane) * 8, p.res_ptrs + ic, m_ok ? 8u : 0u);
+#pragma unroll
+      for (int i = 0; i < BN / 32; ++i) {
+        const int n = w.n_base + i * 32 + lane;
+        const bool ok = p.bias && n < p.N;
+        ptx::cp_async4(epi_s + (buf * BN + i * 32 + lane) * 4, ok ? static_cast<const void*>(p.bias + n) : p.out_ptrs,
+                       ok ? 4u : 0u);
+      }
+      ptx::cp_async_commit();
+    };
+    if (static_cast<int>(blockIdx.x) < units) prefetch(blockIdx.x, 0);
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = unit_of(p, u, BN, KT);
       const int acc = j % S::kAcc;
-      // Row pointers are global loads (the per-request blob table): issue
-      // them before waiting for the accumulator so their latency hides
-      // behind this unit's MMAs instead of serialising every epilogue.
-      int n_img = 0, pix = 0;
-      const bool m_ok = row_pixel(p, w.mt, row, n_img, pix);
-      float* out_row = m_ok ? p.out_ptrs[n_img] + p.out_off + static_cast<long>(pix) * p.out_ldc : nullptr;
-      const float* res_row =
-          (m_ok && p.res_ptrs) ? p.res_ptrs[n_img] + p.res_off + static_cast<long>(pix) * p.res_ldc : nullptr;
+      const int buf = j & 1;
+      // Buffer buf ^ 1 was last read by the previous unit's chunks (this
+      // warp, program order); issue the next unit's copies into it, then
+      // wait for this unit's group.
+      if (u + static_cast<int>(gridDim.x) < units) prefetch(u + gridDim.x, buf ^ 1);
+      else ptx::cp_async_commit();  // empty group keeps wait_group<1> exact
+      ptx::cp_async_wait<1>();
+      __syncwarp();
+      const float* bias_st = reinterpret_cast<const float*>(epi_g) + buf * BN;
+      float* out_row = nullptr;
+      const float* res_row = nullptr;
+      {
+        int n_img = 0, pix = 0;
+        if (row_pixel(p, w.mt, row, n_img, pix)) {
+          const auto* tab = reinterpret_cast<const unsigned long long*>(epi_g + kTabB);
+          float* ob = reinterpret_cast<float*>(tab[buf * 32 + lane]);
+          out_row = ob ? ob + p.out_off + static_cast<long>(pix) * p.out_ldc : nullptr;
+          if (p.res_ptrs) {
+            const float* rb = reinterpret_cast<const float*>(tab[64 + buf * 32 + lane]);
+            res_row = rb ? rb + p.res_off + static_cast<long>(pix) * p.res_ldc : nullptr;
+          }
+        }
+        auto* fin = reinterpret_cast<unsigned long long*>(epi_g + kFinB);
+        fin[lane] = reinterpret_cast<unsigned long long>(out_row);
+        fin[32 + lane] = reinterpret_cast<unsigned long long>(res_row);
+      }
+      __syncwarp();
+      // Plain fast path (no residual, no split-K, aligned rows, N % 4 == 0).
+      bool fast = false;
+      if (!p.res_ptrs && p.ksplits == 1) {
+        const bool ok = !out_row || (reinterpret_cast<uintptr_t>(out_row) & 15) == 0;
+        fast = __all_sync(0xffffffffu, ok) && (p.N & 3) == 0 && !(p.debug & 4);
+      }
+      const bool etr = p.trace && threadIdx.x == 128 && blockIdx.x == 0 && j < 32;
+      if (etr) p.trace[3072 + j * 8 + 0] = gtime();
       ptx::mbar_wait(&acc_full[acc], (j / S::kAcc) & 1);
+      if (etr) p.trace[3072 + j * 8 + 1] = gtime();
       ptx::tc_fence_after();
+      if (p.debug & 32) {  // timing experiment: release the accumulator untouched
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&acc_empty[acc]);
+        continue;
+      }
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       if (p.ksplits == 1) {
         // Coalesced epilogue: each warp stages its 32 rows x 32 columns in
@@ -662,8 +732,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
             const int nc = w.n_base + jj * 32 + (lane & 7) * 4;
 #pragma unroll
             for (int rq = 0; rq < 8; ++rq) {
-              const unsigned long long rp =
-                  __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(res_row), rq * 4 + (lane >> 3));
+              const unsigned long long rp = fin_res[rq * 4 + (lane >> 3)];
               const float* rr = reinterpret_cast<const float*>(rp);
               const bool ok = rr && nc + 3 < p.N && (reinterpret_cast<uintptr_t>(rr + nc) & 15) == 0;
               rv[rq] = ok ? __ldg(reinterpret_cast<const float4*>(rr + nc)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -688,15 +757,43 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           const int nc = n0 + cq * 4;       // first column of the chunk
           const bool col_ok = nc < p.N;
           const bool full4 = nc + 3 < p.N;
-          float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (p.bias && full4) b4 = make_float4(__ldg(p.bias + nc), __ldg(p.bias + nc + 1), __ldg(p.bias + nc + 2),
-                                                 __ldg(p.bias + nc + 3));
+          // Zero past N (the prefetch stored 0 there), so no test is needed.
+          const float4 b4 = *reinterpret_cast<const float4*>(bias_st + jj * 32 + cq * 4);
+          if (!RES && fast) {
+            // Branch-free rows: batched LDS (plain loads, reorderable), bias,
+            // activation as a compile-time clamp, st.global.v4.
+            const float* st = reinterpret_cast<const float*>(smem + S::kStagingOffset + ew * 32 * 128);
+            auto rows = [&](auto relu_tag) {
+              constexpr int RELU = decltype(relu_tag)::value;
+#pragma unroll
+              for (int rq = 0; rq < 8; ++rq) {
+                const int rl = rq * 4 + (lane >> 3);
+                float4 x = *reinterpret_cast<const float4*>(st + rl * 32 + ((cq ^ (rl & 7)) << 2));
+                x.x += b4.x; x.y += b4.y; x.z += b4.z; x.w += b4.w;
+                if constexpr (RELU >= 1) {
+                  x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+                }
+                if constexpr (RELU == 2) {
+                  x.x = fminf(x.x, 6.f); x.y = fminf(x.y, 6.f); x.z = fminf(x.z, 6.f); x.w = fminf(x.w, 6.f);
+                }
+                if (p.round_out) {
+                  x.x = ptx::round_tf32(x.x); x.y = ptx::round_tf32(x.y);
+                  x.z = ptx::round_tf32(x.z); x.w = ptx::round_tf32(x.w);
+                }
+                const unsigned long long op = fin_out[rl];
+                if (op && col_ok) ptx::stg128(reinterpret_cast<float*>(op) + nc, x);
+              }
+            };
+            if (p.relu == 1) rows(std::integral_constant<int, 1>{});
+            else if (p.relu == 2) rows(std::integral_constant<int, 2>{});
+            else rows(std::integral_constant<int, 0>{});
+            __syncwarp();
+            return;
+          }
           auto store_row = [&](int rq, const float4& r4) {
             const int rl = rq * 4 + (lane >> 3);  // row inside the warp's 32
-            const unsigned long long op =
-                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(out_row), rl);
-            const unsigned long long rp =
-                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(res_row), rl);
+            const unsigned long long op = fin_out[rl];
+            const unsigned long long rp = fin_res[rl];
             if (!op || !col_ok || (p.debug & 4)) return;
             float4 x = ptx::lds128(stage + rl * 128 + ((cq ^ (rl & 7)) << 4));
             float* dst = reinterpret_cast<float*>(op) + nc;
@@ -720,7 +817,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
               *reinterpret_cast<float4*>(dst) = x;
             } else {
               const float xs[4] = {x.x, x.y, x.z, x.w};
-              for (int q = 0; q < 4 && nc + q < p.N; ++q) dst[q] = epilogue_op(p, xs[q], nc + q, rr);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (nc + q < p.N) dst[q] = epilogue_op(p, xs[q], nc + q, rr);
             }
           };
           if constexpr (RES) {
@@ -738,7 +837,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           for (int jj = 0; jj < BN / 32; ++jj) chunk(jj, std::true_type{});
         } else {
 #pragma unroll 1
-          for (int jj = 0; jj < BN / 32; ++jj) chunk(jj, std::false_type{});
+          for (int jj = 0; jj < BN / 32; ++jj) {
+            chunk(jj, std::false_type{});
+            if (etr && jj < 6) p.trace[3072 + j * 8 + 2 + jj] = gtime();
+          }
         }
       } else {
         // Split-K: park the raw partial tile; once all splits of the tile
