@@ -696,12 +696,23 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
         fin[32 + lane] = reinterpret_cast<unsigned long long>(res_row);
       }
       __syncwarp();
-      // Plain fast path (no residual, no split-K, aligned rows, N % 4 == 0).
+      // Fast path (no split-K, 16-byte aligned rows, N % 4 == 0).
       bool fast = false;
-      if (!p.res_ptrs && p.ksplits == 1) {
-        const bool ok = !out_row || (reinterpret_cast<uintptr_t>(out_row) & 15) == 0;
-        fast = __all_sync(0xffffffffu, ok) && (p.N & 3) == 0 && !(p.debug & 4);
+      if (p.ksplits == 1) {
+        const bool ok = (reinterpret_cast<uintptr_t>(out_row) & 15) == 0 &&
+                        (reinterpret_cast<uintptr_t>(res_row) & 15) == 0 && (!p.res_ptrs || !out_row || res_row);
+        fast = __all_sync(0xffffffffu, ok) && (p.N & 3) == 0 && !(p.debug & 4) && !(p.res_ptrs && (p.debug & 8));
       }
+      // Residual rows: this lane's row segment of a 32-column chunk into L1
+      // one chunk ahead (the quads are read right after the TMEM load).
+      auto prefetch_res = [&](int c) {
+        const int n0 = w.n_base + c * 32;
+        if (res_row && n0 < p.N && !(p.debug & 64)) {
+          ptx::prefetch_l1(res_row + n0);
+          ptx::prefetch_l1(res_row + min(n0 + 31, p.N - 1));
+        }
+      };
+      if (p.ksplits == 1) prefetch_res(0);
       const bool etr = p.trace && threadIdx.x == 128 && blockIdx.x == 0 && j < 32;
       if (etr) p.trace[3072 + j * 8 + 0] = gtime();
       ptx::mbar_wait(&acc_full[acc], (j / S::kAcc) & 1);
@@ -729,6 +740,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           // without a residual).
           [[maybe_unused]] float4 rv[8];
           if constexpr (RES) {
+            if (jj + 1 < BN / 32) prefetch_res(jj + 1);
             const int nc = w.n_base + jj * 32 + (lane & 7) * 4;
 #pragma unroll
             for (int rq = 0; rq < 8; ++rq) {
@@ -759,7 +771,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           const bool full4 = nc + 3 < p.N;
           // Zero past N (the prefetch stored 0 there), so no test is needed.
           const float4 b4 = *reinterpret_cast<const float4*>(bias_st + jj * 32 + cq * 4);
-          if (!RES && fast) {
+          if (fast) {
             // Branch-free rows: batched LDS (plain loads, reorderable), bias,
             // activation as a compile-time clamp, st.global.v4.
             const float* st = reinterpret_cast<const float*>(smem + S::kStagingOffset + ew * 32 * 128);
@@ -770,6 +782,9 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
                 const int rl = rq * 4 + (lane >> 3);
                 float4 x = *reinterpret_cast<const float4*>(st + rl * 32 + ((cq ^ (rl & 7)) << 2));
                 x.x += b4.x; x.y += b4.y; x.z += b4.z; x.w += b4.w;
+                if constexpr (RES) {
+                  x.x += rv[rq].x; x.y += rv[rq].y; x.z += rv[rq].z; x.w += rv[rq].w;
+                }
                 if constexpr (RELU >= 1) {
                   x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
                 }
