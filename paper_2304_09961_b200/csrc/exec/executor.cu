@@ -145,6 +145,42 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
       if (!wm.ok) throw std::runtime_error("window tensor maps failed for " + op.name);
     }
   }
+  // Tap-row mode for the stems (default; BS_CONV_TAPROW=0 disables): one K
+  // tile per filter row, so the A gather is one contiguous 128-byte segment
+  // per output pixel and K tile. Weights re-laid to match.
+  {
+    const char* tr_env = std::getenv("BS_CONV_TAPROW");
+    const bool use_tr = !(tr_env && tr_env[0] == '0');
+    taps_.resize(suite_.nets.size());
+    std::vector<float> pool;
+    std::vector<std::pair<std::size_t, std::size_t>> where;
+    for (std::size_t n = 0; n < suite_.nets.size() && use_tr; ++n) {
+      const NetDef& net = suite_.nets[n];
+      taps_[n].resize(net.ops.size());
+      for (std::size_t i = 0; i < net.ops.size(); ++i) {
+        const OpDef& op = net.ops[i];
+        if (op.kind != OpKind::conv || op.out.C > 128 || !conv_tap_rows_eligible(op.in.C, op.KW)) continue;
+        if (n < wins_.size() && i < wins_[n].size() && wins_[n][i].ok) continue;
+        TapRowMap& tm = taps_[n][i];
+        tm.w_off = pool.size();
+        pool.resize(pool.size() + static_cast<std::size_t>(op.out.C) * op.KH * 32);
+        conv_tap_row_weights(suite_.weights.data() + op.w_off, op.out.C, op.Kpad, op.KH, op.KW, op.in.C,
+                             pool.data() + tm.w_off);
+        where.emplace_back(n, i);
+      }
+    }
+    if (!pool.empty()) {
+      ck(cudaMalloc(&d_tap_weights_, pool.size() * sizeof(float)), "tap-row weights");
+      ck(cudaMemcpy(d_tap_weights_, pool.data(), pool.size() * sizeof(float), cudaMemcpyHostToDevice),
+         "tap-row weights H2D");
+    }
+    for (const auto& [n, i] : where) {
+      const OpDef& op = suite_.nets[n].ops[i];
+      TapRowMap& tm = taps_[n][i];
+      tm.ok = encode_weight_map(&tm.wmap, d_tap_weights_ + tm.w_off, op.out.C, op.KH * 32);
+      if (!tm.ok) throw std::runtime_error("tap-row weight map failed for " + op.name);
+    }
+  }
   // One activation tensor map per conv input (the slot space never moves).
   // BS_CONV_TMA=1: feed conv activations by TMA boxes wherever the geometry
   // allows (default: cp.async gather; see DESIGN.md §4 for the ingest limits).
@@ -188,6 +224,7 @@ Executor::~Executor() {
   }
   cudaFree(d_weights_);
   cudaFree(d_win_weights_);
+  cudaFree(d_tap_weights_);
   cudaFree(arena_);
   cudaFree(scratch_ptrs_);
   cudaFree(flush_);
@@ -288,6 +325,12 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
         else if (ni < amaps_.size() && oi < amaps_[ni].size() && amaps_[ni][oi].ok)
           conv_use_act_map(p, amaps_[ni][oi].map, amaps_[ni][oi].geom, arena_, static_cast<long>(slot_floats_),
                            total_slots_);
+        else if (ni < taps_.size() && oi < taps_[ni].size() && taps_[ni][oi].ok) {
+          p.tap_rows = 1;
+          p.Kpad = op.KH * 32;
+          p.wmap = taps_[ni][oi].wmap;
+          p.wgt = d_tap_weights_ + taps_[ni][oi].w_off;
+        }
       }
       e = launch_conv_tc(p, *ws_, stream_);
       break;

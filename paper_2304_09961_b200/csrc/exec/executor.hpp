@@ -175,6 +175,13 @@ class Executor {
   };
   std::vector<std::vector<WinMap>> wins_;         // [net][op] window-mode maps (spatial convs)
   float* d_win_weights_ = nullptr;                // chunk-major copies of the spatial conv weights
+  struct TapRowMap {
+    bool ok = false;
+    CUtensorMap wmap{};
+    std::size_t w_off = 0;  // into d_tap_weights_
+  };
+  std::vector<std::vector<TapRowMap>> taps_;      // [net][op] tap-row mode (stems)
+  float* d_tap_weights_ = nullptr;                // (kh, kw < 32 / Cin, ci) copies of the stem weights
   long total_slots_ = 0;
   ConvWorkspace conv_ws_;                         // split-K partials + tile counters (serving stream)
   ConvWorkspace side_ws_;                         // the same for the client-prefix side stream

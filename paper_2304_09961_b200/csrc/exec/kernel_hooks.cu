@@ -111,6 +111,20 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
           goto done;
         }
         conv_use_act_map(p, amap, g, din, static_cast<long>(in_img), nimg);
+      } else if (d->N <= 128 && conv_tap_rows_eligible(d->Cin, d->KW) &&
+                 !(std::getenv("BS_CONV_TAPROW") && std::getenv("BS_CONV_TAPROW")[0] == '0')) {
+        // Tap-row mode (the executor's rule for the stems): re-laid weights.
+        std::vector<float> hw(static_cast<size_t>(d->N) * d->KH * 32);
+        conv_tap_row_weights(w_host, d->N, Kpad, d->KH, d->KW, d->Cin, hw.data());
+        CK(cudaMalloc(&dwin, hw.size() * sizeof(float)));
+        CK(cudaMemcpy(dwin, hw.data(), hw.size() * sizeof(float), cudaMemcpyHostToDevice));
+        if (!encode_weight_map(&p.wmap, dwin, d->N, d->KH * 32)) {
+          rc = bs_fail(BS_ECUDA, "tap-row weight map failed");
+          goto done;
+        }
+        p.tap_rows = 1;
+        p.Kpad = d->KH * 32;
+        p.wgt = dwin;
       }
     }
     unsigned long long* trace = nullptr;

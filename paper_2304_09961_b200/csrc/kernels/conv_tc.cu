@@ -161,6 +161,24 @@ void conv_window_weights(const float* w, int N, int Kpad_src, int KH, int KW, in
   }
 }
 
+bool conv_tap_rows_eligible(int Cin, int KW) {
+  if (Cin != 4 && Cin != 8 && Cin != 16) return false;
+  const int taps = conv_tc::kBK / Cin;
+  return KW <= taps && KW + 1 >= taps;
+}
+
+void conv_tap_row_weights(const float* w, int N, int Kpad_src, int KH, int KW, int Cin, float* out) {
+  const int taps = conv_tc::kBK / Cin;
+  for (int n = 0; n < N; ++n) {
+    float* o = out + static_cast<std::size_t>(n) * KH * conv_tc::kBK;
+    const float* src = w + static_cast<std::size_t>(n) * Kpad_src;
+    for (int kh = 0; kh < KH; ++kh)
+      for (int kw = 0; kw < taps; ++kw)
+        for (int ci = 0; ci < Cin; ++ci)
+          o[(kh * taps + kw) * Cin + ci] = kw < KW ? src[(kh * KW + kw) * Cin + ci] : 0.f;
+  }
+}
+
 bool encode_window_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
                        long slot_floats, const WinGeom& wg) {
   const EncodeTiledFn encode = encode_fn();
@@ -212,6 +230,8 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   const int sms = sm_count();
   const int KT = p.Kpad / conv_tc::kBK;
   if (p.a_tma && (p.G < 1 || p.G > 4 || p.Wb * p.Hb * p.G != conv_tc::kBM || p.a_g % 4 || p.Cin % p.a_g))
+    return cudaErrorInvalidValue;
+  if (p.tap_rows && (p.a_tma || !conv_tap_rows_eligible(p.Cin, p.KW) || p.Kpad != p.KH * conv_tc::kBK))
     return cudaErrorInvalidValue;
   if (p.a_win && (!p.a_tma || bn > 128 || p.G * p.win_img_bytes > conv_tc::kWinBytes || p.ktpc <= 0 ||
                   p.Kpad != (p.Cin / p.a_g) * p.ktpc * conv_tc::kBK))

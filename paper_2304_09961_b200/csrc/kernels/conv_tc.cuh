@@ -94,6 +94,11 @@ struct ConvParams {
   int Win, Hin, ktpc;
   int win_img_bytes;            // smem stride between the G image windows (1024-aligned)
   int win_tx_bytes;             // bytes one image window box delivers
+  // Tap-row mode (Cin * 32 / Cin taps = one K tile per filter row): K order
+  // (kh, kw < 32 / Cin, ci) with zero weights past KW, Kpad = KH * 32. Each
+  // output pixel's A row of a K tile is 32 / Cin consecutive input pixels
+  // (128 contiguous bytes); only the input row advances per K tile.
+  int tap_rows;
   int debug;                    // experiment switches (0 in production; BS_CONV_DEBUG)
   CUtensorMap wmap_wide;        // weights with a 256-row box (N > 128), used for 128 x 256 tiles
   int has_wide;
@@ -538,7 +543,63 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     const float* dummy = p.wgt;
     const bool aligned = p.Cin % kBK == 0;
     int it = 0;  // ring position across units
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    if (p.tap_rows) {
+      // One K tile per filter row kh: this thread's 16 bytes are tap kw,
+      // channels ci..ci+3 of input pixel (ho*s - pad + kh, wo*s - pad + kw).
+      const int kw = (c * 4) / p.Cin, ci = c * 4 - kw * p.Cin;
+      const long hstride = static_cast<long>(p.W) * p.in_ldc;
+      // A 128-row tile spans at most two images when HoWo >= 128: their
+      // pointers are loaded one unit ahead (a load at the top of the unit
+      // stalls the first K tile, and this producer paces the stems).
+      const bool two = HoWo >= kBM;
+      const float* nx0 = nullptr;
+      const float* nx1 = nullptr;
+      auto img_ptrs = [&](int u) {
+        const int n0 = unit_of(p, u, BN, KT).m_base / HoWo;
+        nx0 = p.in_ptrs[n0];
+        nx1 = p.in_ptrs[min(n0 + 1, p.nimg - 1)];
+      };
+      if (two && static_cast<int>(blockIdx.x) < units) img_ptrs(blockIdx.x);
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = unit_of(p, u, BN, KT);
+        const float* p0 = nx0;
+        const float* p1 = nx1;
+        if (two && u + static_cast<int>(gridDim.x) < units) img_ptrs(u + gridDim.x);
+        const int nfirst = w.m_base / HoWo;
+        const float* base[8];
+        int h0[8];
+        bool ok_w[8];
+        uint32_t doff[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int m = w.m_base + r0 + 16 * i;
+          const int mm = m < M ? m : 0;
+          const int n = mm / HoWo;
+          const int rem = mm - n * HoWo;
+          const int ho = rem / p.Wo;
+          const int wo = rem - ho * p.Wo;
+          const int wi = wo * p.stride - p.pad + kw;
+          h0[i] = ho * p.stride - p.pad;
+          ok_w[i] = m < M && kw < p.KW && wi >= 0 && wi < p.W;
+          const float* img = two ? (n == nfirst ? p0 : p1) : p.in_ptrs[n];
+          base[i] = img + p.in_off + (static_cast<long>(h0[i]) * p.W + wi) * p.in_ldc + ci;
+          doff[i] = swz(r0 + 16 * i, c);
+        }
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+          const int s = it % RA;
+          if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
+          const uint32_t a_tile = smem_base + s * S::kABytes;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const bool ok = ok_w[i] && static_cast<unsigned>(h0[i] + kt) < static_cast<unsigned>(p.H);
+            ptx::cp_async16(a_tile + doff[i], ok ? base[i] + kt * hstride : dummy, ok ? 16u : 0u);
+          }
+          ptx::cp_async_arrive_noinc(&ra_full[s]);
+          if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
+        }
+      }
+    }
+    for (int u = blockIdx.x; u < units && !p.tap_rows; u += gridDim.x) {
       const Unit w = unit_of(p, u, BN, KT);
       const float* row_base[8];
       int row_h[8], row_w[8];
@@ -619,6 +680,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
             ptx::cp_async16(a_tile + doff[i], srcp, ok ? 16u : 0u);
           }
           ptx::cp_async_arrive_noinc(&ra_full[s]);
+          if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
           k0 += kBK;
           ci += kBK;
           while (ci >= p.Cin) {
@@ -1024,6 +1086,10 @@ bool conv_window_geometry(int Cin, int KH, int KW, int Ho, int Wo, int stride, W
 // matrix: out[N][Kwin].
 void conv_window_weights(const float* w, int N, int Kpad_src, int KH, int KW, int Cin, const WinGeom& wg,
                          float* out);
+// Tap-row mode eligibility (Cin 4 / 8 / 16 and at most one padded tap per
+// filter row: the stems) and the matching weight layout out[N][KH * 32].
+bool conv_tap_rows_eligible(int Cin, int KW);
+void conv_tap_row_weights(const float* w, int N, int Kpad_src, int KH, int KW, int Cin, float* out);
 // Window tensor map: {C, W, H, slot} box {g, Win, Hin, 1}.
 bool encode_window_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
                        long slot_floats, const WinGeom& wg);

@@ -76,6 +76,13 @@ CASES = [
     dict(nimg=2, H=56, W=56, Cin=24, N=144, KH=1, KW=1, stride=1, pad=0),
     dict(nimg=2, H=112, W=112, Cin=16, N=32, KH=3, KW=3, stride=2, pad=1),
     dict(nimg=5, H=8, W=8, Cin=64, N=64, KH=3, KW=3, stride=1, pad=1),
+    # Tap-row mode (stems: one K tile per filter row): tiles inside one image
+    # and across images (HoWo < 128 and not a multiple of 128), Cin 8 / 16.
+    dict(nimg=3, H=100, W=100, Cin=4, N=64, KH=7, KW=7, stride=2, pad=3),
+    dict(nimg=5, H=16, W=16, Cin=4, N=64, KH=7, KW=7, stride=2, pad=3),
+    dict(nimg=3, H=30, W=30, Cin=8, N=48, KH=3, KW=3, stride=1, pad=1),
+    dict(nimg=2, H=20, W=20, Cin=16, N=32, KH=1, KW=1, stride=1, pad=0),
+    dict(nimg=2, H=9, W=11, Cin=16, N=40, KH=2, KW=2, stride=1, pad=0),
 ]
 
 
@@ -90,6 +97,12 @@ def test_conv_channel_slices_residual_relu():
     err = run_conv(2, 14, 14, 64, 96, 3, 3, 1, 1, in_ldc=256, in_coff=64, out_ldc=512,
                    out_coff=128, residual=True, relu=1)
     assert err < TOL
+
+
+@pytest.mark.gpu
+def test_conv_stem_tap_rows_residual_relu():
+    # Full-width stem rows (224 -> 112, two images per some tiles) with a residual.
+    assert run_conv(2, 224, 224, 4, 64, 7, 7, 2, 3, residual=True, relu=1) < TOL
 
 
 @pytest.mark.gpu

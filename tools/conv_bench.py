@@ -6,15 +6,15 @@ import ctypes as C
 import numpy as np
 from paper_2304_09961_b200._native import bs_conv_desc, check, exec_lib, fptr
 
-def bench(nimg, H, Cin, N, k, pad, in_ldc=None, reps=50, split=1, res=False):
+def bench(nimg, H, Cin, N, k, pad, in_ldc=None, reps=50, split=1, res=False, stride=1):
     in_ldc = in_ldc or Cin
-    Ho = H + 2 * pad - k + 1
+    Ho = (H + 2 * pad - k) // stride + 1
     x = np.random.default_rng(0).standard_normal((nimg, H, H, in_ldc)).astype(np.float32)
     K = k * k * Cin; Kp = (K + 31) // 32 * 32
     w = np.zeros((N, Kp), np.float32); b = np.zeros(N, np.float32)
     out = np.zeros((nimg, Ho, Ho, N), np.float32)
     r = np.random.default_rng(1).standard_normal((nimg, Ho, Ho, N)).astype(np.float32) if res else None
-    d = bs_conv_desc(H=H, W=H, Cin=Cin, Ho=Ho, Wo=Ho, KH=k, KW=k, stride=1, pad=pad, N=N, in_ldc=in_ldc, in_coff=0,
+    d = bs_conv_desc(H=H, W=H, Cin=Cin, Ho=Ho, Wo=Ho, KH=k, KW=k, stride=stride, pad=pad, N=N, in_ldc=in_ldc, in_coff=0,
                      out_ldc=N, out_coff=0, res_ldc=N, res_coff=0, relu=1, round_out=0, split=split)
     ms = C.c_float()
     check(exec_lib().bs_kernel_conv(d, nimg, fptr(x), fptr(w), fptr(b), fptr(r) if res else None, fptr(out), reps, C.byref(ms)))
