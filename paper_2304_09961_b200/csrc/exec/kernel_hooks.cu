@@ -159,6 +159,9 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
         std::fprintf(stderr, "  unit %2d epi wait %7lld acc_full %7lld chunks %7lld %7lld %7lld %7lld\n", j,
                      rel(h[3072 + j * 8]), rel(h[3073 + j * 8]), rel(h[3074 + j * 8]), rel(h[3075 + j * 8]),
                      rel(h[3076 + j * 8]), rel(h[3077 + j * 8]));
+      for (int j = 0; j < 32 && h[3400 + j * 4]; ++j)
+        std::fprintf(stderr, "  producer unit %2d top %7lld setup %7lld\n", j, rel(h[3400 + j * 4]),
+                     rel(h[3401 + j * 4]));
       p.trace = nullptr;
       cudaFree(trace);
     }

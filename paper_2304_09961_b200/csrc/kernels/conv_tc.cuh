@@ -543,59 +543,100 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     const float* dummy = p.wgt;
     const bool aligned = p.Cin % kBK == 0;
     int it = 0;  // ring position across units
+    // (image, ho, wo) of rows r0 + 16 i of the tile at m_base: one division
+    // pair, then a 16-row walk (was 16 divisions per unit; the unit switch
+    // stalled the stem's producer ~1.4 us). Rows past M: ok = false, image 0.
+    auto walk_rows = [&](int m_base, int (&n)[8], int (&ho)[8], int (&wo)[8], bool (&ok)[8]) {
+      int m = m_base + r0;
+      int nn = m / HoWo;
+      const int rem = m - nn * HoWo;
+      int h = rem / p.Wo;
+      int ww = rem - h * p.Wo;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        ok[i] = m < M;
+        n[i] = ok[i] ? nn : 0;
+        ho[i] = h;
+        wo[i] = ww;
+        m += 16;
+        ww += 16;
+        while (ww >= p.Wo) {
+          ww -= p.Wo;
+          if (++h == p.Ho) {
+            h = 0;
+            ++nn;
+          }
+        }
+      }
+    };
     if (p.tap_rows) {
-      // One K tile per filter row kh: this thread's 16 bytes are tap kw,
-      // channels ci..ci+3 of input pixel (ho*s - pad + kh, wo*s - pad + kw).
-      const int kw = (c * 4) / p.Cin, ci = c * 4 - kw * p.Cin;
+      // One K tile per filter row kh. Warp pw owns tile rows 32 pw .. +31:
+      // lane l works out row 32 pw + l (image, input row / column origin)
+      // once per unit, and the 8 row groups a lane copies (rows 4 i + l / 8,
+      // 16 bytes = tap kw, channels ci..ci+3) come from shuffles; the row
+      // state was computed 8x redundantly per lane before (~480 SASS per
+      // unit on the producer, which paces the stems).
+      const int pw = warp;
+      const int cc = lane & 7;
+      const int kw = (cc * 4) / p.Cin, ci = cc * 4 - kw * p.Cin;
       const long hstride = static_cast<long>(p.W) * p.in_ldc;
-      // A 128-row tile spans at most two images when HoWo >= 128: their
-      // pointers are loaded one unit ahead (a load at the top of the unit
-      // stalls the first K tile, and this producer paces the stems).
-      const bool two = HoWo >= kBM;
-      const float* nx0 = nullptr;
-      const float* nx1 = nullptr;
-      auto img_ptrs = [&](int u) {
-        const int n0 = unit_of(p, u, BN, KT).m_base / HoWo;
-        nx0 = p.in_ptrs[n0];
-        nx1 = p.in_ptrs[min(n0 + 1, p.nimg - 1)];
+      // Own-row state of the next unit (its image pointer load is issued a
+      // unit ahead of its use).
+      int nx_h0 = 0, nx_w0 = 0;
+      bool nx_ok = false;
+      const float* nx_img = nullptr;
+      auto own_row = [&](int u) {
+        const int m = unit_of(p, u, BN, KT).m_base + 32 * pw + lane;
+        nx_ok = m < M;
+        const int mm = nx_ok ? m : 0;
+        const int n = mm / HoWo;
+        const int rem = mm - n * HoWo;
+        const int ho = rem / p.Wo;
+        nx_h0 = ho * p.stride - p.pad;
+        nx_w0 = (rem - ho * p.Wo) * p.stride - p.pad;
+        nx_img = p.in_ptrs[n] + p.in_off;
       };
-      if (two && static_cast<int>(blockIdx.x) < units) img_ptrs(blockIdx.x);
+      uint32_t doff[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) doff[i] = swz(32 * pw + 4 * i + (lane >> 3), cc);
+      if (static_cast<int>(blockIdx.x) < units) own_row(blockIdx.x);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit w = unit_of(p, u, BN, KT);
-        const float* p0 = nx0;
-        const float* p1 = nx1;
-        if (two && u + static_cast<int>(gridDim.x) < units) img_ptrs(u + gridDim.x);
-        const int nfirst = w.m_base / HoWo;
+        const int my_h0 = nx_h0, my_w0 = nx_w0;
+        const bool my_ok = nx_ok;
+        const float* my_img = nx_img;
+        if (u + static_cast<int>(gridDim.x) < units) own_row(u + gridDim.x);
         const float* base[8];
         int h0[8];
         bool ok_w[8];
-        uint32_t doff[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int m = w.m_base + r0 + 16 * i;
-          const int mm = m < M ? m : 0;
-          const int n = mm / HoWo;
-          const int rem = mm - n * HoWo;
-          const int ho = rem / p.Wo;
-          const int wo = rem - ho * p.Wo;
-          const int wi = wo * p.stride - p.pad + kw;
-          h0[i] = ho * p.stride - p.pad;
-          ok_w[i] = m < M && kw < p.KW && wi >= 0 && wi < p.W;
-          const float* img = two ? (n == nfirst ? p0 : p1) : p.in_ptrs[n];
-          base[i] = img + p.in_off + (static_cast<long>(h0[i]) * p.W + wi) * p.in_ldc + ci;
-          doff[i] = swz(r0 + 16 * i, c);
+          const int src = 4 * i + (lane >> 3);
+          const int rh = __shfl_sync(0xffffffffu, my_h0, src);
+          const int wi = __shfl_sync(0xffffffffu, my_w0, src) + kw;
+          const bool rok = __shfl_sync(0xffffffffu, static_cast<int>(my_ok), src) != 0;
+          const float* img = reinterpret_cast<const float*>(
+              __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_img), src));
+          h0[i] = rh + w.kt0;
+          ok_w[i] = rok && kw < p.KW && wi >= 0 && wi < p.W;
+          base[i] = img + (static_cast<long>(h0[i]) * p.W + wi) * p.in_ldc + ci;
         }
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % RA;
           if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
           const uint32_t a_tile = smem_base + s * S::kABytes;
+          // The copies read the loop-carried row pointers (an out-of-image
+          // tap keeps its address and copies 0 bytes: cp.async zero-fills
+          // without reading).
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const bool ok = ok_w[i] && static_cast<unsigned>(h0[i] + kt) < static_cast<unsigned>(p.H);
-            ptx::cp_async16(a_tile + doff[i], ok ? base[i] + kt * hstride : dummy, ok ? 16u : 0u);
+            const bool ok = ok_w[i] && static_cast<unsigned>(h0[i]) < static_cast<unsigned>(p.H);
+            ptx::cp_async16(a_tile + doff[i], base[i], ok ? 16u : 0u);
+            base[i] += hstride;
+            ++h0[i];
           }
           ptx::cp_async_arrive_noinc(&ra_full[s]);
-          if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
+          if (p.trace && threadIdx.x == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
         }
       }
     }
@@ -604,18 +645,15 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
       const float* row_base[8];
       int row_h[8], row_w[8];
       bool row_ok[8];
+      {
+        int rn[8], rho[8], rwo[8];
+        walk_rows(w.m_base, rn, rho, rwo, row_ok);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int m = w.m_base + r0 + 16 * i;
-        row_ok[i] = m < M;
-        const int mm = row_ok[i] ? m : 0;
-        const int n = mm / HoWo;
-        const int rem = mm - n * HoWo;
-        const int ho = rem / p.Wo;
-        const int wo = rem - ho * p.Wo;
-        row_h[i] = ho * p.stride - p.pad;
-        row_w[i] = wo * p.stride - p.pad;
-        row_base[i] = p.in_ptrs[n] + p.in_off;
+        for (int i = 0; i < 8; ++i) {
+          row_h[i] = rho[i] * p.stride - p.pad;
+          row_w[i] = rwo[i] * p.stride - p.pad;
+          row_base[i] = p.in_ptrs[rn[i]] + p.in_off;
+        }
       }
       uint32_t doff[8];
 #pragma unroll
@@ -634,7 +672,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           for (int i = 0; i < 8; ++i) {
             const int h = row_h[i] + kh, ww = row_w[i] + kw;
             const bool ok = row_ok[i] && h >= 0 && h < p.H && ww >= 0 && ww < p.W;
-            src[i] = ok ? row_base[i] + (h * p.W + ww) * p.in_ldc + c * 4 : dummy;
+            src[i] = row_base[i] + (h * p.W + ww) * p.in_ldc + c * 4 + ci;  // 0 bytes when !ok
             nbytes[i] = ok ? 16u : 0u;
           }
         };
@@ -643,19 +681,25 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           const int s = it % RA;
           if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
           const uint32_t a_tile = smem_base + s * S::kABytes;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) ptx::cp_async16(a_tile + doff[i], src[i] + ci, nbytes[i]);
+          // src[i] already points at this K tile (ci folded in): each LDGSTS
+          // reads a loop-carried register, never a reused temporary.
+          ptx::cp_async16x8(a_tile + doff[0], 16 * 128, src, nbytes);
           ptx::cp_async_arrive_noinc(&ra_full[s]);
           if (p.trace && t == 0 && it == 0) p.trace[8 + 4 * blockIdx.x + 2] = gtime();
           if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
           ci += kBK;
-          if (ci == p.Cin && kt + 1 < w.kt1) {
-            ci = 0;
-            if (++kw == p.KW) {
-              kw = 0;
-              ++kh;
+          if (ci == p.Cin) {
+            if (kt + 1 < w.kt1) {
+              ci = 0;
+              if (++kw == p.KW) {
+                kw = 0;
+                ++kh;
+              }
+              set_tap();
             }
-            set_tap();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) src[i] += kBK;
           }
         }
       } else {

@@ -65,6 +65,32 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
                "r"(src_bytes)
                : "memory");
 }
+// Eight 16-byte async copies in one statement: the eight source addresses
+// are distinct live registers, so no copy waits for an earlier LDGSTS to
+// release a reused address register.
+__device__ __forceinline__ void cp_async16x8(uint32_t dst0, uint32_t step, const float* (&src)[8],
+                                             const uint32_t (&nb)[8]) {
+  asm volatile(
+      "cp.async.cg.shared.global [%0], [%2], 16, %10;\n\t"
+      "add.u32 %0, %0, %1;\n\t"
+      "cp.async.cg.shared.global [%0], [%3], 16, %11;\n\t"
+      "add.u32 %0, %0, %1;\n\t"
+      "cp.async.cg.shared.global [%0], [%4], 16, %12;\n\t"
+      "add.u32 %0, %0, %1;\n\t"
+      "cp.async.cg.shared.global [%0], [%5], 16, %13;\n\t"
+      "add.u32 %0, %0, %1;\n\t"
+      "cp.async.cg.shared.global [%0], [%6], 16, %14;\n\t"
+      "add.u32 %0, %0, %1;\n\t"
+      "cp.async.cg.shared.global [%0], [%7], 16, %15;\n\t"
+      "add.u32 %0, %0, %1;\n\t"
+      "cp.async.cg.shared.global [%0], [%8], 16, %16;\n\t"
+      "add.u32 %0, %0, %1;\n\t"
+      "cp.async.cg.shared.global [%0], [%9], 16, %17;"
+      : "+r"(dst0)
+      : "r"(step), "l"(src[0]), "l"(src[1]), "l"(src[2]), "l"(src[3]), "l"(src[4]), "l"(src[5]), "l"(src[6]),
+        "l"(src[7]), "r"(nb[0]), "r"(nb[1]), "r"(nb[2]), "r"(nb[3]), "r"(nb[4]), "r"(nb[5]), "r"(nb[6]), "r"(nb[7])
+      : "memory");
+}
 // Small async copies (4 / 8 bytes, zero-filled when src_bytes == 0).
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
