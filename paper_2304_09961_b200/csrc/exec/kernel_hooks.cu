@@ -1,3 +1,4 @@
+#include <algorithm>
 // Kernel-level C-ABI hooks: run one layer kernel on host buffers. Used by the
 // per-kernel parity tests (tests/test_kernels_gpu.py) and by the latency
 // profiler; the serving path goes through bs_step instead.
@@ -146,6 +147,15 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
       for (int b = 0; b < 254; ++b)
         if (h[8 + 4 * b] && h[8 + 4 * b] < t0) t0 = h[8 + 4 * b];
       auto rel = [&](unsigned long long v) { return v ? static_cast<long long>(v - t0) : -1LL; };
+      {
+        long long smin = 1LL << 60, smax = 0, emin = 1LL << 60, emax = 0;
+        int nb = 0;
+        for (int b = 0; b < 254 && h[8 + 4 * b]; ++b, ++nb) {
+          smin = std::min(smin, rel(h[8 + 4 * b])); smax = std::max(smax, rel(h[8 + 4 * b]));
+          emin = std::min(emin, rel(h[11 + 4 * b])); emax = std::max(emax, rel(h[11 + 4 * b]));
+        }
+        std::fprintf(stderr, "  ctas %d start [%lld, %lld] end [%lld, %lld]\n", nb, smin, smax, emin, emax);
+      }
       for (int b = 0; b < 254 && h[8 + 4 * b]; ++b)
         if (b < 2)
           std::fprintf(stderr, "  cta %3d start %7lld setup %7lld firstA %7lld end %7lld\n", b, rel(h[8 + 4 * b]),

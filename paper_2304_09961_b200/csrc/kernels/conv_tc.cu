@@ -28,8 +28,7 @@ cudaError_t launch_bn(const ConvParams& p, int grid, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  conv_tc::conv_tc_kernel<BN, SPLIT><<<grid, S::kThreads, S::kTotal, stream>>>(p);
-  return cudaGetLastError();
+  return pdl::launch(conv_tc::conv_tc_kernel<BN, SPLIT>, dim3(grid), dim3(S::kThreads), S::kTotal, stream, p);
 }
 
 }  // namespace

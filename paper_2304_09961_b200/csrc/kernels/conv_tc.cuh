@@ -42,6 +42,7 @@
 
 #include <cuda.h>
 
+#include "pdl.cuh"
 #include "ptx.cuh"
 
 namespace bs200 {
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
   const uint32_t smem_base = ptx::smem_u32(smem);
   // trace: [8 + 4 b + {0 start, 1 setup done, 2 first A issued, 3 end}]
   if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x] = gtime();
+  pdl::launch_dependents();  // pdl.cuh: the next layer kernel may be scheduled
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RA; ++s) {
@@ -296,6 +298,11 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Everything above overlapped the previous kernel's tail (PDL). The weight
+  // TMA warp reads only immutable weights and starts at once; every other
+  // role touches activations / blob tables / the split-K workspace and waits
+  // for the previous kernel to complete.
+  if (warp != 9) pdl::wait();
   if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x + 1] = gtime();
 
   // Converter: thread = one A row (TMEM lane). Reads its 128-byte row of a
@@ -716,13 +723,19 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
           const uint32_t a_tile = smem_base + s * S::kABytes;
           const bool k_ok = k0 < p.K;
+          // All 8 addresses first (fresh IMAD.WIDE pairs), then one 8-copy
+          // statement: interleaving address math with the copies made every
+          // address wait for the previous LDGSTS to release a reused pair.
+          const float* srcs[8];
+          uint32_t nb[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int h = row_h[i] + kh, ww = row_w[i] + kw;
             const bool ok = k_ok && row_ok[i] && h >= 0 && h < p.H && ww >= 0 && ww < p.W;
-            const float* srcp = ok ? row_base[i] + (h * p.W + ww) * p.in_ldc + ci : dummy;
-            ptx::cp_async16(a_tile + doff[i], srcp, ok ? 16u : 0u);
+            srcs[i] = row_base[i] + (h * p.W + ww) * p.in_ldc + ci;  // 0 bytes when !ok
+            nb[i] = ok ? 16u : 0u;
           }
+          ptx::cp_async16x8(a_tile + doff[0], 16 * 128, srcs, nb);
           ptx::cp_async_arrive_noinc(&ra_full[s]);
           if (p.trace && t == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
           k0 += kBK;

@@ -1,6 +1,7 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include "pdl.cuh"
 #include "ptx.cuh"
 #include "simple_ops.cuh"
 
@@ -24,6 +25,8 @@ __device__ __forceinline__ float4 max4(float4 a, float4 b) {
 // One thread per (image, output pixel, 4 channels); 32-bit index math
 // (every pooled tensor of a 90-request batch has < 2^31 float4s).
 __global__ void maxpool_kernel(const PoolParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
   const int C4 = p.C >> 2;
   const int total = p.nimg * p.Ho * p.Wo * C4;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -50,6 +53,8 @@ __global__ void maxpool_kernel(const PoolParams p) {
 // so they are in flight together.
 template <int K>
 __global__ void __launch_bounds__(256) maxpool_unrolled_kernel(const PoolParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
   const int C4 = p.C >> 2;
   const int total = p.nimg * p.Ho * p.Wo * C4;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -85,6 +90,8 @@ __global__ void __launch_bounds__(256) maxpool_unrolled_kernel(const PoolParams 
 // take consecutive channel quads (coalesced 16-byte accesses).
 template <int S>
 __global__ void __launch_bounds__(256) maxpool3_block_kernel(const PoolParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
   constexpr int IN = S + 3;  // input rows / cols of a 2x2 output block (windows [0,3) and [S,S+3))
   const int C4 = p.C >> 2;
   const int Bw = (p.Wo + 1) >> 1, Bh = (p.Ho + 1) >> 1;
@@ -141,6 +148,8 @@ __global__ void __launch_bounds__(256) maxpool3_block_kernel(const PoolParams p)
 // element once per output row (3 loads per output instead of 9) and the
 // index math is per row, not per output.
 __global__ void maxpool_rows_kernel(const PoolParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
   const int C4 = p.C >> 2;
   const long total = static_cast<long>(p.nimg) * p.Ho * C4;
   const float4 ninf = make_float4(-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX);
@@ -176,6 +185,8 @@ __global__ void maxpool_rows_kernel(const PoolParams p) {
 
 // One thread per (image, 4 channels); sums the H*W pixels in fp32.
 __global__ void avgpool_kernel(const AvgPoolParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
   const int C4 = p.C >> 2;
   const long total = static_cast<long>(p.nimg) * C4;
   const float inv = 1.0f / static_cast<float>(p.HW);
@@ -210,6 +221,8 @@ __device__ __forceinline__ float act(float x, int relu) {
 }
 
 __global__ void dwconv_kernel(const DwParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
   const int C4 = p.C >> 2;
   const long total = static_cast<long>(p.nimg) * p.Ho * p.Wo * C4;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
@@ -258,6 +271,8 @@ __global__ void dwconv_kernel(const DwParams p) {
 // 25 at stride 2, against 36) and the nine weight quads once per block.
 template <int S>
 __global__ void __launch_bounds__(256) dwconv3_block_kernel(const DwParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
   constexpr int IN = S + 3;
   const int C4 = p.C >> 2;
   const int Bw = (p.Wo + 1) >> 1, Bh = (p.Ho + 1) >> 1;
@@ -326,6 +341,8 @@ __global__ void __launch_bounds__(256) dwconv3_block_kernel(const DwParams p) {
 
 // One warp per image: max, sum of exp, normalise.
 __global__ void softmax_kernel(const SoftmaxParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= p.nimg) return;
@@ -342,6 +359,8 @@ __global__ void softmax_kernel(const SoftmaxParams p) {
 }
 
 __global__ void expand_rgb_kernel(const float* __restrict__ rgb, float* __restrict__ dst, int hw) {
+  pdl::launch_dependents();
+  pdl::wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += gridDim.x * blockDim.x) {
     const float r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
     reinterpret_cast<float4*>(dst)[i] = make_float4(r, g, b, 0.f);
@@ -351,53 +370,58 @@ __global__ void expand_rgb_kernel(const float* __restrict__ rgb, float* __restri
 }  // namespace
 
 cudaError_t launch_expand_rgb(const float* rgb, float* dst, int hw, cudaStream_t s) {
-  expand_rgb_kernel<<<grid_for(hw), kThreads, 0, s>>>(rgb, dst, hw);
-  return cudaGetLastError();
+  cudaError_t e = cudaSuccess;
+  e = pdl::launch(expand_rgb_kernel, dim3(grid_for(hw)), dim3(kThreads), 0, s, rgb, dst, hw);
+  return e;
 }
 
 cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
   if (p.C % 4 || p.k > 3) return cudaErrorInvalidValue;
   const long rows = static_cast<long>(p.nimg) * p.Ho * (p.C / 4);
   // The row-sliding form loads each input once per row but serialises a
   // row's outputs; it pays only when rows alone fill the GPU several times.
   const long outs = static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4);
   if (p.stride == 1 && rows >= 148L * 2048 * 2)
-    maxpool_rows_kernel<<<grid_for(rows), kThreads, 0, s>>>(p);
+    e = pdl::launch(maxpool_rows_kernel, dim3(grid_for(rows)), dim3(kThreads), 0, s, p);
   else if (p.k == 3 && (p.stride == 1 || p.stride == 2) && !std::getenv("BS_POOL_SIMPLE")) {
     const long blocks = static_cast<long>(p.nimg) * ((p.Ho + 1) / 2) * ((p.Wo + 1) / 2) * (p.C / 4);
-    if (p.stride == 1) maxpool3_block_kernel<1><<<grid_for(blocks), kThreads, 0, s>>>(p);
-    else maxpool3_block_kernel<2><<<grid_for(blocks), kThreads, 0, s>>>(p);
+    if (p.stride == 1) e = pdl::launch(maxpool3_block_kernel<1>, dim3(grid_for(blocks)), dim3(kThreads), 0, s, p);
+    else e = pdl::launch(maxpool3_block_kernel<2>, dim3(grid_for(blocks)), dim3(kThreads), 0, s, p);
   } else if (p.k == 3)
-    maxpool_unrolled_kernel<3><<<grid_for(outs), kThreads, 0, s>>>(p);
+    e = pdl::launch(maxpool_unrolled_kernel<3>, dim3(grid_for(outs)), dim3(kThreads), 0, s, p);
   else if (p.k == 2)
-    maxpool_unrolled_kernel<2><<<grid_for(outs), kThreads, 0, s>>>(p);
+    e = pdl::launch(maxpool_unrolled_kernel<2>, dim3(grid_for(outs)), dim3(kThreads), 0, s, p);
   else
-    maxpool_kernel<<<grid_for(outs), kThreads, 0, s>>>(p);
-  return cudaGetLastError();
+    e = pdl::launch(maxpool_kernel, dim3(grid_for(outs)), dim3(kThreads), 0, s, p);
+  return e;
 }
 
 cudaError_t launch_avgpool(const AvgPoolParams& p, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
   if (p.C % 4) return cudaErrorInvalidValue;
-  avgpool_kernel<<<grid_for(static_cast<long>(p.nimg) * (p.C / 4)), kThreads, 0, s>>>(p);
-  return cudaGetLastError();
+  e = pdl::launch(avgpool_kernel, dim3(grid_for(static_cast<long>(p.nimg) * (p.C / 4))), dim3(kThreads), 0, s, p);
+  return e;
 }
 
 cudaError_t launch_dwconv(const DwParams& p, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
   if (p.C % 4) return cudaErrorInvalidValue;
   const long blocks = static_cast<long>(p.nimg) * ((p.Ho + 1) / 2) * ((p.Wo + 1) / 2) * (p.C / 4);
   if (p.stride == 1 && !std::getenv("BS_DW_SIMPLE"))
-    dwconv3_block_kernel<1><<<grid_for(blocks), kThreads, 0, s>>>(p);
+    e = pdl::launch(dwconv3_block_kernel<1>, dim3(grid_for(blocks)), dim3(kThreads), 0, s, p);
   else if (p.stride == 2 && !std::getenv("BS_DW_SIMPLE"))
-    dwconv3_block_kernel<2><<<grid_for(blocks), kThreads, 0, s>>>(p);
+    e = pdl::launch(dwconv3_block_kernel<2>, dim3(grid_for(blocks)), dim3(kThreads), 0, s, p);
   else
-    dwconv_kernel<<<grid_for(static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4)), kThreads, 0, s>>>(p);
-  return cudaGetLastError();
+    e = pdl::launch(dwconv_kernel, dim3(grid_for(static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4))), dim3(kThreads), 0, s, p);
+  return e;
 }
 
 cudaError_t launch_softmax(const SoftmaxParams& p, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
   const int blocks = (p.nimg * 32 + kThreads - 1) / kThreads;
-  softmax_kernel<<<blocks, kThreads, 0, s>>>(p);
-  return cudaGetLastError();
+  e = pdl::launch(softmax_kernel, dim3(blocks), dim3(kThreads), 0, s, p);
+  return e;
 }
 
 }  // namespace bs200
