@@ -456,6 +456,7 @@ void Executor::wait_slot_free(int index, cudaStream_t st) {
   const std::size_t i = static_cast<std::size_t>(index);
   if (!slot_free_pending_[i]) return;
   ck(cudaStreamWaitEvent(st, slot_free_ev_[i], 0), "wait slot free");
+  pdl::suppress_next();
   slot_free_pending_[i] = 0;
 }
 
@@ -495,6 +496,7 @@ void Executor::drop(std::int64_t id) {
   if (it->second.pending_ready) {
     // a pending input copy / prefix must finish before the slot can be reused
     ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
+    pdl::suppress_next();
   }
   const std::size_t idx = static_cast<std::size_t>(it->second.index);
   ck(cudaEventRecord(slot_free_ev_[idx], stream_), "slot free rec");
@@ -528,6 +530,7 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     if (it == slot_of_.end()) throw std::logic_error("step member not admitted: " + std::to_string(id));
     if (it->second.pending_ready) {
       ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
+      pdl::suppress_next();
       it->second.pending_ready = false;
     }
   }
@@ -551,6 +554,7 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     if (it == slot_of_.end()) continue;  // dropped meanwhile
     if (it->second.pending_ready) {
       ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
+      pdl::suppress_next();
       it->second.pending_ready = false;
     }
     auto rb = ride_of_.find(r.id);

@@ -13,7 +13,14 @@
 //     workspace); only immutable inputs (weights, bias) may be touched before.
 //     Since every kernel waits, completion stays ordered along the stream and
 //     kernel k+2 transitively sees kernel k.
-// Outside a PDL launch both instructions are no-ops. BS_PDL=0 disables it.
+// Outside a PDL launch both instructions are no-ops.
+//
+// Opt-in (BS_PDL=1). Measured on B200: per-layer timings improve at small
+// batches (GoogLeNet b=8 layer sum 919 -> 853 us, b=90 unchanged), but the
+// live serving loop (bench.py) shows intermittent stalls with it -- capacity
+// probes become non-monotonic and the e2e (H2D admission) rate fell from
+// 29.8k to 16.3k req/s -- so the default launch stays stream-serialised
+// until that interaction is understood.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -32,10 +39,21 @@ __device__ __forceinline__ void wait() { asm volatile("griddepcontrol.wait;" :::
 inline bool enabled() {
   static const bool on = [] {
     const char* e = std::getenv("BS_PDL");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
+
+// A launch right after a cross-stream event wait (admission ready events,
+// slot-release events) or on the admission copy stream goes without PDL:
+// measured, PDL launches behind cudaStreamWaitEvent made the e2e (H2D
+// admission) serving path ~3x slower. Host-thread local, consumed by the next
+// launch on this thread.
+inline bool& suppressed() {
+  thread_local bool s = false;
+  return s;
+}
+inline void suppress_next() { suppressed() = true; }
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
@@ -47,7 +65,9 @@ cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = enabled() ? 1 : 0;
+  const bool skip = suppressed();
+  suppressed() = false;
+  attr[0].val.programmaticStreamSerializationAllowed = enabled() && !skip ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);

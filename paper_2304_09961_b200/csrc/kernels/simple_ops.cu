@@ -371,6 +371,7 @@ __global__ void expand_rgb_kernel(const float* __restrict__ rgb, float* __restri
 
 cudaError_t launch_expand_rgb(const float* rgb, float* dst, int hw, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
+  pdl::suppress_next();  // admission copy stream: after an H2D copy / event wait
   e = pdl::launch(expand_rgb_kernel, dim3(grid_for(hw)), dim3(kThreads), 0, s, rgb, dst, hw);
   return e;
 }
