@@ -291,6 +291,16 @@ def run_ours(a, ws, rank, local) -> dict | None:
         roof["avg_launch_us"] = round(conv["ms"] / conv["launches"] * 1000, 2)
         roof["peak_source"] = f"{pk['source']}: tf32 = bf16_tflops_sustained / 2; hbm_gbs measured copy"
         roof["traffic"] = ncu_traffic()
+        # The TF32 MMA rate measured on this part (profiles/r01/micro_b200.txt,
+        # tools/micro/mma_micro.cu: one 128x128x8 MMA per 64 cycles per SM) at
+        # the SM clock sampled during the run. 2xTF32 issues two MMAs per
+        # algorithmic MAC, so tensor_pipe_frac = 2 * achieved / this rate.
+        import torch
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        mma_rate = 2 * 128 * 128 * 8 / 64 * sms * mhz * 1e6 / 1e12
+        roof["tf32_mma_rate_measured"] = round(mma_rate, 1)
+        roof["tensor_pipe_frac"] = round(2 * ach / mma_rate, 4) if tensor_bound else None
         total_ms = sum(v["ms"] for v in stats.values())
         roof["share_of_device_time"] = round(conv["ms"] / total_ms, 4) if total_ms else None
 
