@@ -201,6 +201,87 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
       if (!am.ok) throw std::runtime_error("activation tensor map failed for " + op.name);
     }
   }
+  plan_groups();
+}
+
+// Launch order per layer. Two convs of a layer are grouped into one launch
+// when neither reads or writes what the other writes (channel slices of one
+// tensor, or the arena ranges of different tensors, which the planner may
+// alias): the two branch convs of an inception block, or -- by running a
+// pooling op first -- the merged 1x1 conv and the pool projection.
+void Executor::plan_groups() {
+  const char* env = std::getenv("BS_CONV_GROUP");
+  const bool on = !(env && env[0] == '0');
+  plans_.assign(suite_.nets.size(), {});
+  gmaps_.assign(suite_.nets.size(), {});
+  gmap_ok_.assign(suite_.nets.size(), {});
+  for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
+    const NetDef& net = suite_.nets[n];
+    gmaps_[n].resize(net.ops.size());
+    gmap_ok_[n].assign(net.ops.size(), 0);
+    auto overlap = [&](const TRef& x, const TRef& y) {
+      if (x.t < 0 || y.t < 0) return false;
+      if (x.t == y.t) return x.coff < y.coff + y.C && y.coff < x.coff + x.C;
+      const TensorDef& a = net.tensors[static_cast<std::size_t>(x.t)];
+      const TensorDef& b = net.tensors[static_cast<std::size_t>(y.t)];
+      const long ae = a.off + static_cast<long>(a.H) * a.W * a.C, be = b.off + static_cast<long>(b.H) * b.W * b.C;
+      return a.off < be && b.off < ae;
+    };
+    // No ordering constraint between x and y (either may run first / both at once).
+    auto indep = [&](const OpDef& x, const OpDef& y) {
+      return !overlap(x.out, y.in) && !overlap(x.out, y.res) && !overlap(y.out, x.in) && !overlap(y.out, x.res) &&
+             !overlap(x.out, y.out);
+    };
+    auto groupable = [&](int i) {
+      const OpDef& op = net.ops[static_cast<std::size_t>(i)];
+      const auto k = static_cast<std::size_t>(i);
+      return op.kind == OpKind::conv && !(n < taps_.size() && k < taps_[n].size() && taps_[n][k].ok) &&
+             !(n < wins_.size() && k < wins_[n].size() && wins_[n][k].ok) &&
+             !(n < amaps_.size() && k < amaps_[n].size() && amaps_[n][k].ok);
+    };
+    for (const LayerDef& L : net.layers) {
+      std::vector<LayerItem> items;
+      const std::vector<int>& o = L.ops;
+      std::size_t i = 0;
+      while (i < o.size()) {
+        const int a = o[i];
+        if (on && groupable(a)) {
+          if (i + 1 < o.size() && groupable(o[i + 1]) &&
+              indep(net.ops[static_cast<std::size_t>(a)], net.ops[static_cast<std::size_t>(o[i + 1])])) {
+            items.push_back({a, o[i + 1]});
+            i += 2;
+            continue;
+          }
+          if (i + 2 < o.size() && net.ops[static_cast<std::size_t>(o[i + 1])].kind != OpKind::conv &&
+              groupable(o[i + 2]) &&
+              indep(net.ops[static_cast<std::size_t>(a)], net.ops[static_cast<std::size_t>(o[i + 1])]) &&
+              indep(net.ops[static_cast<std::size_t>(a)], net.ops[static_cast<std::size_t>(o[i + 2])])) {
+            items.push_back({o[i + 1], -1});  // the pool runs first
+            items.push_back({a, o[i + 2]});
+            i += 3;
+            continue;
+          }
+        }
+        items.push_back({a, -1});
+        ++i;
+      }
+      // Weight maps at the group's tile width for the narrower conv of a pair.
+      for (const LayerItem& it : items) {
+        if (it.b < 0) continue;
+        const OpDef& x = net.ops[static_cast<std::size_t>(it.a)];
+        const OpDef& y = net.ops[static_cast<std::size_t>(it.b)];
+        const int bn = std::max(conv_tile_n(x.out.C), conv_tile_n(y.out.C));
+        for (int k : {it.a, it.b}) {
+          const OpDef& op = net.ops[static_cast<std::size_t>(k)];
+          if (conv_tile_n(op.out.C) == bn) continue;
+          if (!encode_weight_map(&gmaps_[n][static_cast<std::size_t>(k)], d_weights_ + op.w_off, op.out.C, op.Kpad, bn))
+            throw std::runtime_error("group weight map failed for " + op.name);
+          gmap_ok_[n][static_cast<std::size_t>(k)] = 1;
+        }
+      }
+      plans_[n].push_back(std::move(items));
+    }
+  }
 }
 
 Executor::~Executor() {
@@ -264,6 +345,98 @@ float** Executor::table_alloc(std::size_t n, float*** host_view) {
 
 // ------------------------------------------------------------------ launch
 
+ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch) const {
+  const auto off = [&](const TRef& r) -> long {
+    return r.t < 0 ? 0 : net.tensors[static_cast<std::size_t>(r.t)].off + r.coff;
+  };
+  const auto ldc = [&](const TRef& r) -> int { return r.t < 0 ? 0 : net.tensors[static_cast<std::size_t>(r.t)].C; };
+  const TensorDef& ti = net.tensors[static_cast<std::size_t>(op.in.t)];
+  ConvParams p{};
+  p.wmap = wmaps_[static_cast<std::size_t>(&net - suite_.nets.data())][static_cast<std::size_t>(&op - net.ops.data())];
+  if (op.out.C > 128)
+    conv_add_wide_map(p, wmaps_wide_[static_cast<std::size_t>(&net - suite_.nets.data())]
+                                    [static_cast<std::size_t>(&op - net.ops.data())]);
+  p.nimg = batch;
+  p.H = ti.H;
+  p.W = ti.W;
+  p.Cin = op.in.C;
+  p.Ho = op.Ho;
+  p.Wo = op.Wo;
+  p.KH = op.KH;
+  p.KW = op.KW;
+  p.stride = op.stride;
+  p.pad = op.pad;
+  p.K = op.KH * op.KW * op.in.C;
+  p.Kpad = op.Kpad;
+  p.N = op.out.C;
+  p.in_ptrs = d_ptrs;
+  p.in_off = off(op.in);
+  p.in_ldc = ldc(op.in);
+  p.wgt = d_weights_ + op.w_off;
+  p.bias = d_weights_ + op.b_off;
+  p.out_ptrs = d_ptrs;
+  p.out_off = off(op.out);
+  p.out_ldc = ldc(op.out);
+  p.res_ptrs = op.res.t >= 0 ? d_ptrs : nullptr;
+  p.res_off = off(op.res);
+  p.res_ldc = ldc(op.res);
+  p.relu = op.relu;
+  p.round_out = split_ ? 0 : op.round_out;
+  p.split = split_ ? 1 : 0;
+  {
+    const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
+    const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
+    if (ni < wins_.size() && oi < wins_[ni].size() && wins_[ni][oi].ok)
+      conv_use_window(p, wins_[ni][oi].amap, wins_[ni][oi].wmap, wins_[ni][oi].geom, arena_,
+                      static_cast<long>(slot_floats_), total_slots_);
+    else if (ni < amaps_.size() && oi < amaps_[ni].size() && amaps_[ni][oi].ok)
+      conv_use_act_map(p, amaps_[ni][oi].map, amaps_[ni][oi].geom, arena_, static_cast<long>(slot_floats_),
+                       total_slots_);
+    else if (ni < taps_.size() && oi < taps_[ni].size() && taps_[ni][oi].ok) {
+      p.tap_rows = 1;
+      p.Kpad = op.KH * 32;
+      p.wmap = taps_[ni][oi].wmap;
+      p.wgt = d_tap_weights_ + taps_[ni][oi].w_off;
+    }
+  }
+  return p;
+}
+
+void Executor::launch_group(const NetDef& net, const OpDef& a, const OpDef& b, float* const* d_ptrs, int batch) {
+  const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
+  ConvParams pa = conv_params(net, a, d_ptrs, batch), pb = conv_params(net, b, d_ptrs, batch);
+  const std::size_t ia = static_cast<std::size_t>(&a - net.ops.data()), ib = static_cast<std::size_t>(&b - net.ops.data());
+  if (gmap_ok_[ni][ia]) pa.wmap = gmaps_[ni][ia];
+  if (gmap_ok_[ni][ib]) pb.wmap = gmaps_[ni][ib];
+  LaunchStat st{};
+  const bool sample = stats_on_ && (++stats_seen_ % stats_every_ == 0) && ev_next_ + 2 <= event_pool_.size();
+  if (sample) {
+    st.kind = OpKind::conv;
+    st.batch = batch;
+    st.bytes = op_bytes(net, a, batch) + op_bytes(net, b, batch);
+    st.flops = op_flops(a, batch) + op_flops(b, batch);
+    st.t0 = event_pool_[ev_next_++];
+    st.t1 = event_pool_[ev_next_++];
+    ck(cudaEventRecord(st.t0, stream_), "ev rec");
+  }
+  const cudaError_t e = launch_conv_tc_group(pa, pb, *ws_, stream_);
+  if (e == cudaErrorNotSupported) {  // split-K / wide tiles win at this batch
+    if (sample) {
+      ev_next_ -= 2;
+      --stats_seen_;
+    }
+    launch_op(net, a, d_ptrs, batch);
+    launch_op(net, b, d_ptrs, batch);
+    return;
+  }
+  ck(e, (a.name + "+" + b.name).c_str());
+  ++launches_;
+  if (sample) {
+    ck(cudaEventRecord(st.t1, stream_), "ev rec");
+    stats_.push_back(st);
+  }
+}
+
 void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch) {
   const auto off = [&](const TRef& r) -> long {
     return r.t < 0 ? 0 : net.tensors[static_cast<std::size_t>(r.t)].off + r.coff;
@@ -284,55 +457,7 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
   cudaError_t e = cudaSuccess;
   switch (op.kind) {
     case OpKind::conv: {
-      ConvParams p{};
-      p.wmap = wmaps_[static_cast<std::size_t>(&net - suite_.nets.data())][static_cast<std::size_t>(&op - net.ops.data())];
-      if (op.out.C > 128)
-        conv_add_wide_map(p, wmaps_wide_[static_cast<std::size_t>(&net - suite_.nets.data())]
-                                        [static_cast<std::size_t>(&op - net.ops.data())]);
-      p.nimg = batch;
-      p.H = ti.H;
-      p.W = ti.W;
-      p.Cin = op.in.C;
-      p.Ho = op.Ho;
-      p.Wo = op.Wo;
-      p.KH = op.KH;
-      p.KW = op.KW;
-      p.stride = op.stride;
-      p.pad = op.pad;
-      p.K = op.KH * op.KW * op.in.C;
-      p.Kpad = op.Kpad;
-      p.N = op.out.C;
-      p.in_ptrs = d_ptrs;
-      p.in_off = off(op.in);
-      p.in_ldc = ldc(op.in);
-      p.wgt = d_weights_ + op.w_off;
-      p.bias = d_weights_ + op.b_off;
-      p.out_ptrs = d_ptrs;
-      p.out_off = off(op.out);
-      p.out_ldc = ldc(op.out);
-      p.res_ptrs = op.res.t >= 0 ? d_ptrs : nullptr;
-      p.res_off = off(op.res);
-      p.res_ldc = ldc(op.res);
-      p.relu = op.relu;
-      p.round_out = split_ ? 0 : op.round_out;
-      p.split = split_ ? 1 : 0;
-      {
-        const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
-        const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
-        if (ni < wins_.size() && oi < wins_[ni].size() && wins_[ni][oi].ok)
-          conv_use_window(p, wins_[ni][oi].amap, wins_[ni][oi].wmap, wins_[ni][oi].geom, arena_,
-                          static_cast<long>(slot_floats_), total_slots_);
-        else if (ni < amaps_.size() && oi < amaps_[ni].size() && amaps_[ni][oi].ok)
-          conv_use_act_map(p, amaps_[ni][oi].map, amaps_[ni][oi].geom, arena_, static_cast<long>(slot_floats_),
-                           total_slots_);
-        else if (ni < taps_.size() && oi < taps_[ni].size() && taps_[ni][oi].ok) {
-          p.tap_rows = 1;
-          p.Kpad = op.KH * 32;
-          p.wmap = taps_[ni][oi].wmap;
-          p.wgt = d_tap_weights_ + taps_[ni][oi].w_off;
-        }
-      }
-      e = launch_conv_tc(p, *ws_, stream_);
+      e = launch_conv_tc(conv_params(net, op, d_ptrs, batch), *ws_, stream_);
       break;
     }
     case OpKind::maxpool: {
@@ -370,8 +495,10 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
 void Executor::run_layer(int dnn, int layer, float* const* d_ptrs, int batch) {
   if (batch <= 0) return;
   const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
-  for (int oi : net.layers[static_cast<std::size_t>(layer - 1)].ops)
-    launch_op(net, net.ops[static_cast<std::size_t>(oi)], d_ptrs, batch);
+  for (const LayerItem& it : plans_[static_cast<std::size_t>(dnn)][static_cast<std::size_t>(layer - 1)]) {
+    if (it.b < 0) launch_op(net, net.ops[static_cast<std::size_t>(it.a)], d_ptrs, batch);
+    else launch_group(net, net.ops[static_cast<std::size_t>(it.a)], net.ops[static_cast<std::size_t>(it.b)], d_ptrs, batch);
+  }
 }
 
 // --------------------------------------------------------------- requests

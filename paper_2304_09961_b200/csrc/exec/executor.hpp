@@ -112,6 +112,11 @@ class Executor {
   float* slot_ptr(int index) const { return arena_ + static_cast<std::size_t>(index) * slot_floats_; }
   float** table_alloc(std::size_t n, float*** host_view);
   void launch_op(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch);
+  ConvParams conv_params(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch) const;
+  // Two independent convs of one layer in one persistent launch (falls back
+  // to two launches when the launcher declines: split-K or wide tiles win).
+  void launch_group(const NetDef& net, const OpDef& a, const OpDef& b, float* const* d_ptrs, int batch);
+  void plan_groups();
 
   Suite suite_;
   int device_ = 0;
@@ -181,6 +186,14 @@ class Executor {
     std::size_t w_off = 0;  // into d_tap_weights_
   };
   std::vector<std::vector<TapRowMap>> taps_;      // [net][op] tap-row mode (stems)
+  // Per layer, the launch order: single ops, or (a, b) conv pairs run as one
+  // grouped launch (independent branch convs; BS_CONV_GROUP=0 disables).
+  struct LayerItem {
+    int a = -1, b = -1;
+  };
+  std::vector<std::vector<std::vector<LayerItem>>> plans_;  // [net][layer - 1]
+  std::vector<std::vector<CUtensorMap>> gmaps_;              // [net][op] weights at the group's tile width
+  std::vector<std::vector<char>> gmap_ok_;
   float* d_tap_weights_ = nullptr;                // (kh, kw < 32 / Cin, ci) copies of the stem weights
   long total_slots_ = 0;
   ConvWorkspace conv_ws_;                         // split-K partials + tile counters (serving stream)

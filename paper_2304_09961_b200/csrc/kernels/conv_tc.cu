@@ -18,17 +18,18 @@ int sm_count() {
   return n;
 }
 
-template <int BN, bool SPLIT>
-cudaError_t launch_bn(const ConvParams& p, int grid, cudaStream_t stream) {
+template <int BN, bool SPLIT, bool GROUP>
+cudaError_t launch_bn(const ConvParams& p, const ConvParams& p2, int grid, cudaStream_t stream) {
   using S = conv_tc::Cfg<BN, SPLIT>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc::conv_tc_kernel<BN, SPLIT>,
+    cudaError_t e = cudaFuncSetAttribute(conv_tc::conv_tc_kernel<BN, SPLIT, GROUP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return pdl::launch(conv_tc::conv_tc_kernel<BN, SPLIT>, dim3(grid), dim3(S::kThreads), S::kTotal, stream, p);
+  return pdl::launch(conv_tc::conv_tc_kernel<BN, SPLIT, GROUP>, dim3(grid), dim3(S::kThreads), S::kTotal, stream, p,
+                     p2);
 }
 
 }  // namespace
@@ -222,6 +223,61 @@ void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& g, c
   p.oob_slot = static_cast<int>(slots);
 }
 
+namespace {
+// Split-K cost model: a split unit pays the partial-tile round trip and the
+// cross-CTA wait, worth ~24 K tiles of work (fitted on the GoogLeNet latency
+// table, b = 1..64; knobs BS_CONV_KS_MAX / BS_CONV_KS_OVH). Splits only when
+// the tiles cannot cover the SMs, and keeps every split unit co-resident.
+int choose_ksplits(int tiles, int KT, int bn, int sms, const ConvWorkspace& ws) {
+  int ks = 1;
+  static const int ks_max = std::getenv("BS_CONV_KS_MAX") ? std::atoi(std::getenv("BS_CONV_KS_MAX")) : 16;
+  static const int ks_ovh = std::getenv("BS_CONV_KS_OVH") ? std::atoi(std::getenv("BS_CONV_KS_OVH")) : 24;
+  if (tiles < sms && ws.partials && ws.counters && 2 * tiles <= ws.n_counters) {
+    auto cost = [&](int k) {
+      const int per = (KT + k - 1) / k;
+      const int units = tiles * k;
+      const int waves = (units + sms - 1) / sms;
+      return waves * (per + (k > 1 ? ks_ovh : 3));
+    };
+    int best = cost(1);
+    for (int k = 2; k <= ks_max && tiles * k <= sms && k <= KT; ++k) {
+      if (static_cast<std::size_t>(tiles) * k * conv_tc::kBM * bn > ws.partial_floats) break;
+      const int c = cost(k);
+      if (c < best) {
+        best = c;
+        ks = k;
+      }
+    }
+    const int per = (KT + ks - 1) / ks;
+    ks = (KT + per - 1) / per;
+  }
+  return ks;
+}
+
+cudaError_t launch_dispatch(const ConvParams& p, const ConvParams& p2, int bn, int grid, cudaStream_t stream) {
+  if (p.group_units) {  // grouped launches use tile widths <= 128
+    if (p.split) {
+      if (bn == 32) return launch_bn<32, true, true>(p, p2, grid, stream);
+      if (bn == 64) return launch_bn<64, true, true>(p, p2, grid, stream);
+      return launch_bn<128, true, true>(p, p2, grid, stream);
+    }
+    if (bn == 32) return launch_bn<32, false, true>(p, p2, grid, stream);
+    if (bn == 64) return launch_bn<64, false, true>(p, p2, grid, stream);
+    return launch_bn<128, false, true>(p, p2, grid, stream);
+  }
+  if (p.split) {
+    if (bn == 32) return launch_bn<32, true, false>(p, p2, grid, stream);
+    if (bn == 64) return launch_bn<64, true, false>(p, p2, grid, stream);
+    if (bn == 128) return launch_bn<128, true, false>(p, p2, grid, stream);
+    return launch_bn<256, true, false>(p, p2, grid, stream);
+  }
+  if (bn == 32) return launch_bn<32, false, false>(p, p2, grid, stream);
+  if (bn == 64) return launch_bn<64, false, false>(p, p2, grid, stream);
+  if (bn == 128) return launch_bn<128, false, false>(p, p2, grid, stream);
+  return launch_bn<256, false, false>(p, p2, grid, stream);
+}
+}  // namespace
+
 cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t stream) {
   if (p.Cin % 4 != 0 || p.Kpad % conv_tc::kBK != 0 || p.Kpad < p.K || p.nimg <= 0)
     return cudaErrorInvalidValue;
@@ -248,31 +304,7 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   //   waves(units) * (k tiles per unit + per-unit overhead),
   // with every unit of a split-K launch co-resident (units <= SMs) so the
   // cooperative reduction can wait on its tile's splits.
-  int ks = 1;
-  // Split-K cost model: a split unit pays the partial-tile round trip and the
-  // cross-CTA wait, worth ~24 K tiles of work (fitted on the GoogLeNet
-  // latency table, b = 1..64; knobs BS_CONV_KS_MAX / BS_CONV_KS_OVH).
-  static const int ks_max = std::getenv("BS_CONV_KS_MAX") ? std::atoi(std::getenv("BS_CONV_KS_MAX")) : 16;
-  static const int ks_ovh = std::getenv("BS_CONV_KS_OVH") ? std::atoi(std::getenv("BS_CONV_KS_OVH")) : 24;
-  if (tiles < sms && ws.partials && ws.counters && 2 * tiles <= ws.n_counters) {
-    auto cost = [&](int k) {
-      const int per = (KT + k - 1) / k;
-      const int units = tiles * k;
-      const int waves = (units + sms - 1) / sms;
-      return waves * (per + (k > 1 ? ks_ovh : 3));
-    };
-    int best = cost(1);
-    for (int k = 2; k <= ks_max && tiles * k <= sms && k <= KT; ++k) {
-      if (static_cast<std::size_t>(tiles) * k * conv_tc::kBM * bn > ws.partial_floats) break;
-      const int c = cost(k);
-      if (c < best) {
-        best = c;
-        ks = k;
-      }
-    }
-    const int per = (KT + ks - 1) / ks;
-    ks = (KT + per - 1) / per;
-  }
+  const int ks = choose_ksplits(tiles, KT, bn, sms, ws);
   static const int dbg = std::getenv("BS_CONV_DEBUG") ? std::atoi(std::getenv("BS_CONV_DEBUG")) : 0;
   p.debug = dbg;
   p.ksplits = std::max(1, ks);
@@ -285,16 +317,47 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   if (log)
     std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d tma=%d win=%d box=%dx%dx%d g=%d\n",
                  p.nimg * p.Ho * p.Wo, p.N, p.K, KT, bn, tiles, p.ksplits, grid, p.a_tma, p.a_win, p.Hb, p.Wb, p.G, p.a_g);
-  if (p.split) {
-    if (bn == 32) return launch_bn<32, true>(p, grid, stream);
-    if (bn == 64) return launch_bn<64, true>(p, grid, stream);
-    if (bn == 128) return launch_bn<128, true>(p, grid, stream);
-    return launch_bn<256, true>(p, grid, stream);
+  p.group_units = 0;
+  return launch_dispatch(p, p, bn, grid, stream);
+}
+
+cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, const ConvWorkspace& ws, cudaStream_t stream) {
+  for (const ConvParams* q : {&a, &b})
+    if (q->Cin % 4 != 0 || q->Kpad % conv_tc::kBK != 0 || q->Kpad < q->K || q->nimg <= 0 || q->a_tma ||
+        q->a_win || q->tap_rows || q->split != a.split)
+      return cudaErrorInvalidValue;
+  const int bn = std::max(conv_tile_n(a.N), conv_tile_n(b.N));
+  // Grouping gives up split-K: decline (the caller launches the two convs
+  // separately) when either conv would be split on its own.
+  for (const ConvParams* q : {&a, &b}) {
+    const int qbn = conv_tile_n(q->N);
+    const int tiles = ((q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM) * ((q->N + qbn - 1) / qbn);
+    if (choose_ksplits(tiles, q->Kpad / conv_tc::kBK, qbn, sm_count(), ws) > 1) return cudaErrorNotSupported;
+    ConvParams t = *q;
+    t.m_tiles = (q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM;
+    if (use_wide(t, sm_count())) return cudaErrorNotSupported;  // 128 x 256 tiles beat the group
   }
-  if (bn == 32) return launch_bn<32, false>(p, grid, stream);
-  if (bn == 64) return launch_bn<64, false>(p, grid, stream);
-  if (bn == 128) return launch_bn<128, false>(p, grid, stream);
-  return launch_bn<256, false>(p, grid, stream);
+  static const int dbg = std::getenv("BS_CONV_DEBUG") ? std::atoi(std::getenv("BS_CONV_DEBUG")) : 0;
+  for (ConvParams* q : {&a, &b}) {
+    q->m_tiles = (q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM;
+    q->n_tiles = (q->N + bn - 1) / bn;
+    q->ksplits = 1;
+    q->kt_per_split = q->Kpad / conv_tc::kBK;
+    q->partials = ws.partials;
+    q->counters = ws.counters;
+    q->debug = dbg;
+    q->group_units = 0;
+  }
+  b.trace = a.trace;
+  a.group_units = b.m_tiles * b.n_tiles;
+  const int units = a.m_tiles * a.n_tiles + a.group_units;
+  const int grid = std::min(units, sm_count());
+  static const bool log = std::getenv("BS_CONV_LOG") != nullptr;
+  if (log)
+    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=1 grid=%d tma=0 win=0 group=M%dN%dK%d\n",
+                 a.nimg * a.Ho * a.Wo, a.N, a.K, a.Kpad / conv_tc::kBK, bn, units, grid, b.nimg * b.Ho * b.Wo, b.N,
+                 b.K);
+  return launch_dispatch(a, b, bn, grid, stream);
 }
 
 }  // namespace bs200
