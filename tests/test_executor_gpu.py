@@ -259,3 +259,33 @@ def test_collab_partial_replay_config5():
         assert partial, "no request was split between client and server"
         seen, checked = _check_replay_outputs(ex, out, 9, orcs, per_dnn=3)
         assert checked >= 3
+
+
+def test_grouped_conv_launches_match_ungrouped(monkeypatch):
+    """Independent branch convs of a layer share one persistent launch
+    (executor plan_groups / launch_conv_tc_group): fewer conv launches, the
+    same outputs as separate launches, and oracle parity. Batch 40 exercises
+    both the grouped 28x28 inception layers and the declined groups (split-K
+    wins on the 14x14 / 7x7 layers)."""
+    from paper_2304_09961_b200.executor import Executor
+    ids = list(range(1, 41))
+    probs, launches = {}, {}
+    for g in ("1", "0"):
+        monkeypatch.setenv("BS_CONV_GROUP", g)
+        with Executor("googlenet", max_batch=90, max_requests=64) as ex:
+            for i in ids:
+                ex.admit(i, 0, image_for(ex, 0, i % 5))
+            ex.stats(True)
+            ex.plan(1)
+            ex.step(1, 0, 0, 1, 22, [(i, 1) for i in ids])
+            ex.sync()
+            launches[g] = ex.stats_summary(6550.0, 696.0)["conv_tc"]["launches"]
+            probs[g] = {i: ex.retire(i, 1000) for i in ids}
+            if g == "1":
+                orc = NetOracle(ex.desc, 0, ex.weights())
+                refs = {j: orc.probs(orc.forward(image_for(ex, 0, j))) for j in range(5)}
+    assert launches["1"] < launches["0"]
+    for i in ids:
+        assert rel_err(probs["1"][i], probs["0"][i]) < 1e-5
+        assert rel_err(probs["1"][i], refs[i % 5]) < TOL
+        assert int(np.argmax(probs["1"][i])) == int(np.argmax(refs[i % 5]))
