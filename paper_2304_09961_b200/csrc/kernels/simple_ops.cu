@@ -142,6 +142,67 @@ __global__ void __launch_bounds__(256) maxpool3_block_kernel(const PoolParams p)
   }
 }
 
+// 3x3 max-pool, BH x BW output tile per thread (one channel quad): each of
+// the (BH-1)S+3 input rows is loaded once, folded into the BW column-window
+// maxima and those into the output rows whose window covers it. Stride 1 at
+// 2x4 loads 3 inputs per output (2x2: 4). Opt-in (BS_POOL_BLOCK=24 / 44):
+// measured slower than 2x2 on the GoogLeNet pools at b=90 (stride-1 pool
+// time 474 / 505 / 649 us over 3 passes for 2x2 / 2x4 / 4x4) -- the fewer
+// threads in flight cost more than the saved L2 reads.
+template <int S, int BH, int BW>
+__global__ void __launch_bounds__(256) maxpool3_tile_kernel(const PoolParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
+  constexpr int IH = (BH - 1) * S + 3, IW = (BW - 1) * S + 3;
+  const int C4 = p.C >> 2;
+  const int Bw = (p.Wo + BW - 1) / BW, Bh = (p.Ho + BH - 1) / BH;
+  const int total = p.nimg * Bh * Bw * C4;
+  const float4 ninf = make_float4(-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c4 = i % C4;
+    int r = i / C4;
+    const int bw = r % Bw;
+    r /= Bw;
+    const int bh = r % Bh;
+    const int n = r / Bh;
+    const int oh0 = BH * bh, ow0 = BW * bw;
+    const int h0 = oh0 * S - p.pad, w0 = ow0 * S - p.pad;
+    const float* in = p.in_ptrs[n] + p.in_off + c4 * 4;
+    float4 m[BH][BW];
+#pragma unroll
+    for (int a = 0; a < BH; ++a)
+#pragma unroll
+      for (int b = 0; b < BW; ++b) m[a][b] = ninf;
+#pragma unroll
+    for (int dy = 0; dy < IH; ++dy) {
+      const int h = h0 + dy;
+      const bool hok = h >= 0 && h < p.H;
+      float4 v[IW];
+#pragma unroll
+      for (int dx = 0; dx < IW; ++dx) {
+        const int w = w0 + dx;
+        v[dx] = (hok && w >= 0 && w < p.W) ? __ldg(reinterpret_cast<const float4*>(in + (h * p.W + w) * p.in_ldc))
+                                            : ninf;
+      }
+#pragma unroll
+      for (int b = 0; b < BW; ++b) {
+        const float4 cm = max4(max4(v[b * S], v[b * S + 1]), v[b * S + 2]);
+#pragma unroll
+        for (int a = 0; a < BH; ++a)
+          if (dy >= a * S && dy < a * S + 3) m[a][b] = max4(m[a][b], cm);
+      }
+    }
+    float* out = p.out_ptrs[n] + p.out_off + c4 * 4;
+#pragma unroll
+    for (int a = 0; a < BH; ++a)
+#pragma unroll
+      for (int b = 0; b < BW; ++b) {
+        const int oh = oh0 + a, ow = ow0 + b;
+        if (oh < p.Ho && ow < p.Wo) *reinterpret_cast<float4*>(out + (oh * p.Wo + ow) * p.out_ldc) = m[a][b];
+      }
+  }
+}
+
 // Row-sliding max-pool (k <= 3): a thread owns one output row of 4 channels
 // and walks it left to right; each input column's k-row maximum is computed
 // once and kept in a 3-entry ring, so a stride-1 3x3 pool loads every input
@@ -386,9 +447,20 @@ cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {
   if (p.stride == 1 && rows >= 148L * 2048 * 2)
     e = pdl::launch(maxpool_rows_kernel, dim3(grid_for(rows)), dim3(kThreads), 0, s, p);
   else if (p.k == 3 && (p.stride == 1 || p.stride == 2) && !std::getenv("BS_POOL_SIMPLE")) {
-    const long blocks = static_cast<long>(p.nimg) * ((p.Ho + 1) / 2) * ((p.Wo + 1) / 2) * (p.C / 4);
-    if (p.stride == 1) e = pdl::launch(maxpool3_block_kernel<1>, dim3(grid_for(blocks)), dim3(kThreads), 0, s, p);
-    else e = pdl::launch(maxpool3_block_kernel<2>, dim3(grid_for(blocks)), dim3(kThreads), 0, s, p);
+    // Output tile per thread (BS_POOL_BLOCK = 22 / 24 / 44 for stride 1).
+    const char* be = std::getenv("BS_POOL_BLOCK");  // per launch: tests toggle it
+    const int blk = be ? std::atoi(be) : 22;
+    const auto tiles = [&](int bh, int bw) {
+      return static_cast<long>(p.nimg) * ((p.Ho + bh - 1) / bh) * ((p.Wo + bw - 1) / bw) * (p.C / 4);
+    };
+    if (p.stride == 1 && blk == 24)
+      e = pdl::launch(maxpool3_tile_kernel<1, 2, 4>, dim3(grid_for(tiles(2, 4))), dim3(kThreads), 0, s, p);
+    else if (p.stride == 1 && blk == 44)
+      e = pdl::launch(maxpool3_tile_kernel<1, 4, 4>, dim3(grid_for(tiles(4, 4))), dim3(kThreads), 0, s, p);
+    else if (p.stride == 1)
+      e = pdl::launch(maxpool3_block_kernel<1>, dim3(grid_for(tiles(2, 2))), dim3(kThreads), 0, s, p);
+    else
+      e = pdl::launch(maxpool3_block_kernel<2>, dim3(grid_for(tiles(2, 2))), dim3(kThreads), 0, s, p);
   } else if (p.k == 3)
     e = pdl::launch(maxpool_unrolled_kernel<3>, dim3(grid_for(outs)), dim3(kThreads), 0, s, p);
   else if (p.k == 2)

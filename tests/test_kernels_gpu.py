@@ -153,6 +153,16 @@ def test_maxpool_in_executor_layers(k, stride, pad, ceil, H):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("block", ["22", "24", "44"])
+@pytest.mark.parametrize("H,ceil", [(28, True), (14, True), (10, False), (7, True), (9, False)])
+def test_maxpool_stride1_tiles(block, H, ceil, monkeypatch):
+    """Stride-1 3x3 pools with 2x2 / 2x4 / 4x4 output tiles per thread
+    (BS_POOL_BLOCK), partial tiles at the right / bottom edges."""
+    monkeypatch.setenv("BS_POOL_BLOCK", block)
+    test_maxpool_in_executor_layers(3, 1, 1, ceil, H)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("case", CASES[:4] + CASES[10:], ids=lambda c: "x".join(str(c[k]) for k in ("nimg", "H", "Cin", "N", "KH", "stride")))
 def test_conv_tma_activation_path(case, monkeypatch):
     """TMA activation boxes (BS_CONV_TMA=1) on the same layers as the cp.async gather."""
