@@ -254,18 +254,31 @@ def run_ours(a, ws, rank, local) -> dict | None:
     stats = ex.stats_summary(pk["hbm_gbs"], pk["tf32_tflops"])
     ex.stats(False)
 
-    # ---- e2e: same runs through the C-ABI with H2D inputs / D2H results
-    e2e_completed = 0
-    e2e_ms = 0.0
-    h2d = d2h = 0
-    barrier(ws)
-    for k in range(a.steps):
-        r = ex.serve(job(cap, a.requests, 5000 + k + 97 * rank, h2d=True))
-        e2e_completed += r["completed"]
-        e2e_ms += r["device_ms"]
-        h2d += r["h2d_bytes"]
-        d2h += r["d2h_bytes"]
-    barrier(ws)
+    # ---- e2e: same runs through the C-ABI with H2D inputs / D2H results.
+    # Same metric: served req/s at a rate where the on-time ratio still meets
+    # 0.90. Starts at the device-resident capacity and steps down 7% at a time
+    # when the H2D admission path cannot hold the deadlines there.
+    e2e_cap = cap
+    e2e_steps_down = []
+    for attempt in range(5):
+        e2e_completed = e2e_on = e2e_gen = 0
+        e2e_ms = 0.0
+        h2d = d2h = 0
+        barrier(ws)
+        for k in range(a.steps):
+            r = ex.serve(job(e2e_cap, a.requests, 5000 + k + 97 * rank, h2d=True))
+            e2e_completed += r["completed"]
+            e2e_on += r["on_time"]
+            e2e_gen += r["generated"]
+            e2e_ms += r["device_ms"]
+            h2d += r["h2d_bytes"]
+            d2h += r["d2h_bytes"]
+        barrier(ws)
+        e2e_ratio = allreduce_sum(e2e_on, ws) / max(1.0, allreduce_sum(e2e_gen, ws))
+        if e2e_ratio >= 0.90 or attempt == 4:
+            break
+        e2e_steps_down.append([round(e2e_cap, 1), round(e2e_ratio, 4)])
+        e2e_cap *= 0.93
 
     tot_completed = allreduce_sum(completed, ws)
     tot_gen = allreduce_sum(generated, ws)
@@ -343,6 +356,8 @@ def run_ours(a, ws, rank, local) -> dict | None:
                                                 max(1, sum(s["plans"] for s in sched)), 4),
                          "max": round(max(s["sched_ms_max"] for s in sched), 4)},
         "e2e": {"value": round(e2e_tot / (e2e_t / 1000.0), 2) if e2e_t else 0.0, "unit": UNIT,
+                "offered_rate_per_gpu": round(e2e_cap, 1), "on_time_ratio": round(e2e_ratio, 4),
+                "stepped_down_from": e2e_steps_down,
                 "h2d_bytes_per_step": h2d // max(1, a.steps), "d2h_bytes_per_step": d2h // max(1, a.steps)},
         "gpu_launches": launches,
         "clocks": clocks,

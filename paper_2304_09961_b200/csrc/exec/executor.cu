@@ -617,6 +617,26 @@ void Executor::retire_async(std::int64_t id, float* out, int n) {
   drop(id);  // the slot's next admission waits for this copy (slot_free_ev_)
 }
 
+void Executor::retire_many_async(const std::vector<std::int64_t>& ids, const std::vector<float*>& outs, int n) {
+  for (std::size_t b = 0; b < ids.size(); b += kGatherMax) {
+    GatherParams g{};
+    g.n = 0;
+    g.cnt = n;
+    for (std::size_t i = b; i < ids.size() && i < b + kGatherMax; ++i) {
+      auto it = slot_of_.find(ids[i]);
+      if (it == slot_of_.end()) throw std::logic_error("retire of unknown request " + std::to_string(ids[i]));
+      const NetDef& net = suite_.nets[static_cast<std::size_t>(it->second.dnn)];
+      const TensorDef& t = net.tensors[static_cast<std::size_t>(net.probs_t)];
+      g.cnt = std::min(g.cnt, net.num_classes);
+      g.src[g.n] = it->second.blob + t.off;
+      g.dst[g.n] = outs[i];
+      ++g.n;
+    }
+    ck(launch_gather_out(g, stream_), "retire gather");
+  }
+  for (std::int64_t id : ids) drop(id);  // slot reuse waits for the gather (slot_free_ev_)
+}
+
 void Executor::drop(std::int64_t id) {
   auto it = slot_of_.find(id);
   if (it == slot_of_.end()) return;

@@ -60,6 +60,9 @@ class Executor {
   void admit_rgb(std::int64_t id, int dnn, const float* rgb_pinned);
   void retire(std::int64_t id, float* probs_host, int n, bool logits = false);  // synchronous copy
   void retire_async(std::int64_t id, float* probs_pinned, int n);               // stream-ordered copy + free
+  // Batched retire: one copy-out kernel for all ids (pinned, device-mapped
+  // destinations), then the slots are freed in stream order.
+  void retire_many_async(const std::vector<std::int64_t>& ids, const std::vector<float*>& outs, int n);
   void drop(std::int64_t id);
   bool has(std::int64_t id) const { return slot_of_.count(id) != 0; }
   const float* blob(std::int64_t id) const;

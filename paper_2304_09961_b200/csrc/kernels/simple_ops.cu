@@ -419,6 +419,14 @@ __global__ void softmax_kernel(const SoftmaxParams p) {
   for (int j = lane; j < p.N; j += 32) y[j] = __expf(x[j] - m) * inv;
 }
 
+__global__ void gather_out_kernel(const GatherParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
+  const float* src = p.src[blockIdx.x];
+  float* dst = p.dst[blockIdx.x];
+  for (int j = threadIdx.x; j < p.cnt; j += blockDim.x) dst[j] = src[j];
+}
+
 __global__ void expand_rgb_kernel(const float* __restrict__ rgb, float* __restrict__ dst, int hw) {
   pdl::launch_dependents();
   pdl::wait();
@@ -488,6 +496,12 @@ cudaError_t launch_dwconv(const DwParams& p, cudaStream_t s) {
   else
     e = pdl::launch(dwconv_kernel, dim3(grid_for(static_cast<long>(p.nimg) * p.Ho * p.Wo * (p.C / 4))), dim3(kThreads), 0, s, p);
   return e;
+}
+
+cudaError_t launch_gather_out(const GatherParams& p, cudaStream_t s) {
+  if (p.n <= 0) return cudaSuccess;
+  if (p.n > kGatherMax) return cudaErrorInvalidValue;
+  return pdl::launch(gather_out_kernel, dim3(p.n), dim3(kThreads), 0, s, p);
 }
 
 cudaError_t launch_softmax(const SoftmaxParams& p, cudaStream_t s) {

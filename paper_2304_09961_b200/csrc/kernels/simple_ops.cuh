@@ -56,5 +56,15 @@ cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s);
 cudaError_t launch_avgpool(const AvgPoolParams& p, cudaStream_t s);
 cudaError_t launch_dwconv(const DwParams& p, cudaStream_t s);
 cudaError_t launch_softmax(const SoftmaxParams& p, cudaStream_t s);
+// Result copy-out of up to kGatherMax requests in one launch: request i's
+// cnt floats from src[i] to dst[i] (host-mapped pinned memory under UVA), so
+// a step's finishing requests cost one kernel instead of one DMA each.
+constexpr int kGatherMax = 64;
+struct GatherParams {
+  const float* src[kGatherMax];
+  float* dst[kGatherMax];
+  int n, cnt;
+};
+cudaError_t launch_gather_out(const GatherParams& p, cudaStream_t s);
 
 }  // namespace bs200
