@@ -30,7 +30,14 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   ck(cudaSetDevice(device), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
-  ck(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
+  // Admission stream at the highest priority: its expand kernels are tiny
+  // and gate the next steps (ready events); at high load the serving
+  // stream's persistent kernels otherwise keep them waiting for SMs.
+  {
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    ck(cudaStreamCreateWithPriority(&copy_, cudaStreamNonBlocking, hi), "copy stream");
+  }
   ck(cudaMalloc(&d_weights_, suite_.weights.size() * sizeof(float)), "weights");
   ck(cudaMemcpy(d_weights_, suite_.weights.data(), suite_.weights.size() * sizeof(float), cudaMemcpyHostToDevice),
      "weights H2D");
