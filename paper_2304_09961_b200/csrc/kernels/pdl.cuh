@@ -15,12 +15,13 @@
 //     kernel k+2 transitively sees kernel k.
 // Outside a PDL launch both instructions are no-ops.
 //
-// On by default (BS_PDL=0 disables). Measured on B200: per-layer timings
-// improve at small batches (GoogLeNet b=8 layer sum 919 -> 853 us, b=90
-// unchanged). It first stalled the H2D serving path (e2e 29.8k -> 16.3k
-// req/s): the serving stream's early-scheduled CTAs starved the admission
-// stream's expand kernels of SMs. With the admission stream at the highest
-// priority (executor.cu) both paths hold: bench 37.0k / e2e 36.5k req/s.
+// Opt-in (BS_PDL=1). Measured on B200: per-layer timings improve at small
+// batches (GoogLeNet b=8 layer sum 919 -> 853 us, b=90 unchanged), and with
+// the admission stream at the highest priority config 2 serves the same
+// with it (37.0k / e2e 36.5k req/s), but config 3 (shared-layer riders,
+// ride copies between kernels) drops from 2.5k to 1.4-1.5k req/s with PDL
+// even with no programmatic launch behind a copy, so the default launch
+// stays stream-serialised.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -39,7 +40,7 @@ __device__ __forceinline__ void wait() { asm volatile("griddepcontrol.wait;" :::
 inline bool enabled() {
   static const bool on = [] {
     const char* e = std::getenv("BS_PDL");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
