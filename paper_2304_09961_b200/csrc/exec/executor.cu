@@ -393,6 +393,26 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
   {
     const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
     const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
+    if (static_cast<int>(ni) == tune_net_ && static_cast<int>(oi) == tune_op_) {
+      p.wide_pref = tune_pref_;
+    } else if (!tune_batches_.empty() && ni < wide_pref_.size() && oi < wide_pref_[ni].size() &&
+               !wide_pref_[ni][oi].empty()) {
+      // nearest tuned batch (by ratio)
+      std::size_t best = 0;
+      double bd = 1e30;
+      for (std::size_t t = 0; t < tune_batches_.size(); ++t) {
+        const double d = std::fabs(std::log(static_cast<double>(tune_batches_[t]) / batch));
+        if (d < bd) {
+          bd = d;
+          best = t;
+        }
+      }
+      p.wide_pref = wide_pref_[ni][oi][best];
+    }
+  }
+  {
+    const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
+    const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
     if (ni < wins_.size() && oi < wins_[ni].size() && wins_[ni][oi].ok)
       conv_use_window(p, wins_[ni][oi].amap, wins_[ni][oi].wmap, wins_[ni][oi].geom, arena_,
                       static_cast<long>(slot_floats_), total_slots_);
@@ -806,6 +826,44 @@ void Executor::enable_stats(bool on, int every) {
 void Executor::clear_stats() {
   stats_.clear();
   ev_next_ = 0;
+}
+
+std::string Executor::tune_tiles(const std::vector<int>& batches, int reps) {
+  tune_batches_.clear();
+  wide_pref_.assign(suite_.nets.size(), {});
+  std::vector<int> bs;
+  for (int b : batches)
+    if (b >= 1 && b <= max_batch_) bs.push_back(b);
+  std::sort(bs.begin(), bs.end());
+  std::string log = "[";
+  for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
+    const NetDef& net = suite_.nets[n];
+    wide_pref_[n].assign(net.ops.size(), {});
+    for (int k = 1; k <= net.num_layers(); ++k) {
+      for (int oi : net.layers[static_cast<std::size_t>(k - 1)].ops) {
+        const OpDef& op = net.ops[static_cast<std::size_t>(oi)];
+        if (op.kind != OpKind::conv || op.out.C <= 128) continue;
+        auto& prefs = wide_pref_[n][static_cast<std::size_t>(oi)];
+        prefs.assign(bs.size(), 0);
+        for (std::size_t t = 0; t < bs.size(); ++t) {
+          tune_net_ = static_cast<int>(n);
+          tune_op_ = oi;
+          tune_pref_ = 1;
+          const double tw = profile_layer(static_cast<int>(n), k, bs[t], reps, false);
+          tune_pref_ = 2;
+          const double tn = profile_layer(static_cast<int>(n), k, bs[t], reps, false);
+          tune_net_ = tune_op_ = -1;
+          prefs[t] = tw < 0.97 * tn ? 1 : 2;  // wide only on a clear win
+          char buf[160];
+          std::snprintf(buf, sizeof buf, "%s[\"%s\",%d,%.4f,%.4f]", log.size() > 1 ? "," : "", op.name.c_str(), bs[t],
+                        tw, tn);
+          log += buf;
+        }
+      }
+    }
+  }
+  tune_batches_ = bs;
+  return log + "]";
 }
 
 double Executor::profile_layer(int dnn, int layer, int batch, int reps, bool flush_l2) {

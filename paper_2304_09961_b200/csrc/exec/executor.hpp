@@ -121,6 +121,18 @@ class Executor {
   void launch_group(const NetDef& net, const OpDef& a, const OpDef& b, float* const* d_ptrs, int batch);
   void plan_groups();
 
+ public:
+  // Profile-time autotune of the conv tile width: for every conv with
+  // N > 128 and each batch in `batches`, the layer is timed with that conv on
+  // 128 x 256 and on 128-wide tiles; launches then use the faster width for
+  // the nearest tuned batch. Returns the decisions as JSON text.
+  std::string tune_tiles(const std::vector<int>& batches, int reps);
+
+ private:
+  std::vector<int> tune_batches_;                              // sorted tuned batch sizes
+  std::vector<std::vector<std::vector<signed char>>> wide_pref_;  // [net][op][tuned batch]
+  int tune_net_ = -1, tune_op_ = -1, tune_pref_ = 0;           // override while tuning
+
   Suite suite_;
   int device_ = 0;
   int max_batch_ = 90;

@@ -356,6 +356,8 @@ json measure_profile(Executor& ex, const json& opts) {
   if (std::find(batches.begin(), batches.end(), 1) == batches.end()) batches.insert(batches.begin(), 1);
   const int reps = opts.value("reps", 10);
   const bool flush = opts.value("flush_l2", false);
+  json tuned = nullptr;
+  if (opts.value("tune_tiles", false)) tuned = json::parse(ex.tune_tiles(batches, std::max(3, reps / 2)));
   json comps = json::array();
   for (std::size_t c = 0; c < s.components.size(); ++c) {
     // measure a component inside the first DNN that contains it
@@ -386,7 +388,9 @@ json measure_profile(Executor& ex, const json& opts) {
     for (int c : n.components) stages.push_back(s.components[static_cast<std::size_t>(c)].id);
     dnns.push_back({{"id", n.name}, {"stages", stages}});
   }
-  return {{"max_batch", ex.max_batch()}, {"components", comps}, {"dnns", dnns}};
+  json prof = {{"max_batch", ex.max_batch()}, {"components", comps}, {"dnns", dnns}};
+  if (!tuned.is_null()) prof["tile_tune"] = tuned;  // [op, batch, ms wide, ms narrow] (extra key; opt-in)
+  return prof;
 }
 
 }  // namespace bs200

@@ -48,6 +48,8 @@ bool use_wide(const ConvParams& p, int sms) {
   const char* env = std::getenv("BS_CONV_BN256");  // read per launch (tests toggle it)
   if (!p.has_wide || p.a_win || (env && env[0] == '0')) return false;
   if (env && env[0] == '2') return true;
+  if (p.wide_pref == 1) return true;
+  if (p.wide_pref == 2) return false;
   const int narrow = (p.N + 127) / 128, wide = (p.N + 255) / 256;
   return p.N > 128 && p.K >= 512 && wide * 1.8 < narrow && p.m_tiles * wide * 10 >= sms * 9;
 }

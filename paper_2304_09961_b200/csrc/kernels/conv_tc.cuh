@@ -105,6 +105,9 @@ struct ConvParams {
   // branch convs of an inception block), so one persistent launch covers
   // both and the small one stops paying a launch + pipeline fill of its own.
   int group_units;
+  // Tile-width preference from the executor's profile-time autotune:
+  // 0 = launcher rule, 1 = 128 x 256 tiles (needs has_wide), 2 = 128-wide.
+  int wide_pref;
   int debug;                    // experiment switches (0 in production; BS_CONV_DEBUG)
   CUtensorMap wmap_wide;        // weights with a 256-row box (N > 128), used for 128 x 256 tiles
   int has_wide;

@@ -184,9 +184,13 @@ class Executor:
         _check(_lib().bs_profile_layer(self._h, dnn, layer, batch, reps, int(flush_l2), C.byref(ms)))
         return ms.value
 
-    def profile_table(self, batches=(1, 2, 4, 8, 16, 32, 64, 90), reps: int = 10, flush_l2: bool = False) -> dict:
+    def profile_table(self, batches=(1, 2, 4, 8, 16, 32, 64, 90), reps: int = 10, flush_l2: bool = False,
+                      tune_tiles: bool = False) -> dict:
+        """Measured h_k(b) table in the reference schema. tune_tiles: first
+        autotune each N > 128 conv's tile width per batch (kept for later
+        launches; decisions returned under "tile_tune")."""
         out = C.c_void_p()
-        opts = json.dumps({"batches": list(batches), "reps": reps, "flush_l2": flush_l2})
+        opts = json.dumps({"batches": list(batches), "reps": reps, "flush_l2": flush_l2, "tune_tiles": tune_tiles})
         _check(_lib().bs_profile_table(self._h, opts.encode(), C.byref(out)))
         return json.loads(_take_string(out))
 
