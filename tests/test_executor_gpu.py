@@ -289,3 +289,25 @@ def test_grouped_conv_launches_match_ungrouped(monkeypatch):
         assert rel_err(probs["1"][i], probs["0"][i]) < 1e-5
         assert rel_err(probs["1"][i], refs[i % 5]) < TOL
         assert int(np.argmax(probs["1"][i])) == int(np.argmax(refs[i % 5]))
+
+
+def test_tile_autotune_keeps_parity():
+    """profile_table(tune_tiles=True) times every N > 128 conv on both tile
+    widths per batch; later launches use the faster one. Outputs still match
+    the oracle, and the decisions are reported per (op, batch)."""
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("resnet50", max_batch=90, max_requests=48) as ex:
+        prof = ex.profile_table(batches=(8, 32), reps=3, tune_tiles=True)
+        tune = prof["tile_tune"]
+        assert tune and all(len(x) == 4 and x[1] in (1, 8, 32) and x[2] > 0 and x[3] > 0 for x in tune)  # b = 1 always profiled
+        orc = NetOracle(ex.desc, 0, ex.weights())
+        n_layers = len(ex.desc["nets"][0]["layers"])
+        ids = list(range(1, 33))
+        for i in ids:
+            ex.admit(i, 0, image_for(ex, 0, i % 3))
+        ex.plan(1)
+        ex.step(1, 0, 0, 1, n_layers, [(i, 1) for i in ids])
+        refs = {j: orc.probs(orc.forward(image_for(ex, 0, j))) for j in range(3)}
+        for i in ids:
+            p = ex.retire(i, 1000)
+            assert rel_err(p, refs[i % 3]) < TOL and int(np.argmax(p)) == int(np.argmax(refs[i % 3]))
