@@ -227,13 +227,15 @@ void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& g, c
 
 namespace {
 // Split-K cost model: a split unit pays the partial-tile round trip and the
-// cross-CTA wait, worth ~24 K tiles of work (fitted on the GoogLeNet latency
-// table, b = 1..64; knobs BS_CONV_KS_MAX / BS_CONV_KS_OVH). Splits only when
-// the tiles cannot cover the SMs, and keeps every split unit co-resident.
+// cross-CTA wait, worth ~60 K tiles of work (refit on the GoogLeNet and
+// ResNet-50 layer sums at b = 1 / 4 / 16 after the epilogue and grouping
+// changes: 24 -> 60 is -13% / -17% / -12% on GoogLeNet, +3% / -1% / -2% on
+// ResNet-50; knobs BS_CONV_KS_MAX / BS_CONV_KS_OVH). Splits only when the
+// tiles cannot cover the SMs, and keeps every split unit co-resident.
 int choose_ksplits(int tiles, int KT, int bn, int sms, const ConvWorkspace& ws) {
   int ks = 1;
   static const int ks_max = std::getenv("BS_CONV_KS_MAX") ? std::atoi(std::getenv("BS_CONV_KS_MAX")) : 16;
-  static const int ks_ovh = std::getenv("BS_CONV_KS_OVH") ? std::atoi(std::getenv("BS_CONV_KS_OVH")) : 24;
+  static const int ks_ovh = std::getenv("BS_CONV_KS_OVH") ? std::atoi(std::getenv("BS_CONV_KS_OVH")) : 60;
   if (tiles < sms && ws.partials && ws.counters && 2 * tiles <= ws.n_counters) {
     auto cost = [&](int k) {
       const int per = (KT + k - 1) / k;
