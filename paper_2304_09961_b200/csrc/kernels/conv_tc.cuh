@@ -108,6 +108,7 @@ struct ConvParams {
   // Tile-width preference from the executor's profile-time autotune:
   // 0 = launcher rule, 1 = 128 x 256 tiles (needs has_wide), 2 = 128-wide.
   int wide_pref;
+  int n_minor;                  // unit order (see unit_of)
   int debug;                    // experiment switches (0 in production; BS_CONV_DEBUG)
   CUtensorMap wmap_wide;        // weights with a 256-row box (N > 128), used for 128 x 256 tiles
   int has_wide;
@@ -187,8 +188,10 @@ __device__ __forceinline__ Unit unit_of(const ConvParams& p, int u, int BN, int 
   Unit w;
   w.split = u % p.ksplits;
   w.tile = u / p.ksplits;
-  const int mt = w.tile % p.m_tiles;  // consecutive tiles share a weight slice
-  const int nt = w.tile / p.m_tiles;
+  // m-minor: consecutive tiles share a weight slice; n-minor: the N tiles of
+  // an M tile run back to back, so its activations are re-read from L2.
+  const int mt = p.n_minor ? w.tile / p.n_tiles : w.tile % p.m_tiles;
+  const int nt = p.n_minor ? w.tile % p.n_tiles : w.tile / p.m_tiles;
   w.mt = mt;
   w.m_base = mt * kBM;
   w.n_base = nt * BN;
