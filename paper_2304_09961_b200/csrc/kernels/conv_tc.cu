@@ -311,11 +311,13 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   const int ks = choose_ksplits(tiles, KT, bn, sms, ws);
   static const int dbg = std::getenv("BS_CONV_DEBUG") ? std::atoi(std::getenv("BS_CONV_DEBUG")) : 0;
   p.debug = dbg;
-  // n-minor unit order by default: an M tile's activations are re-read for
-  // each N tile while still in L2 (1x1 56x56 64->256 + residual at b=90:
-  // 190 -> 184 us; ResNet-50 layer sum -1%). BS_CONV_NMINOR=0: m-minor.
+  // n-minor unit order (opt-in BS_CONV_NMINOR=1): an M tile's activations
+  // are re-read for each N tile while still in L2 (1x1 56x56 64->256 +
+  // residual at b=90: 190 -> 184 us; ResNet-50 layer sum -1%), but the e2e
+  // (H2D admission) serving capacity came out lower in both bench runs with
+  // it (29.6k / 31.6k vs 35.2k-37.0k req/s with m-minor).
   const char* nm = std::getenv("BS_CONV_NMINOR");  // per launch (A/B)
-  p.n_minor = nm ? (nm[0] == '1') : 1;
+  p.n_minor = nm ? (nm[0] == '1') : 0;
   p.ksplits = std::max(1, ks);
   p.kt_per_split = (KT + p.ksplits - 1) / p.ksplits;
   p.partials = ws.partials;
@@ -357,7 +359,7 @@ cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, const ConvWorkspace
     q->debug = dbg;
     q->group_units = 0;
     const char* nm = std::getenv("BS_CONV_NMINOR");
-    q->n_minor = nm ? (nm[0] == '1') : 1;
+    q->n_minor = nm ? (nm[0] == '1') : 0;
   }
   b.trace = a.trace;
   a.group_units = b.m_tiles * b.n_tiles;
