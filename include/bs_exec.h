@@ -101,6 +101,9 @@ int bs_sync(bs_handle* h);
 /* ----------------------------------------------------------- measurement */
 
 int bs_profile_layer(bs_handle* h, int dnn, int layer, int batch, int reps, int flush_l2, double* ms);
+/* Layers [from, to] at one batch (scratch blobs), ms per pass: ms3[0] synchronised per pass (host launch
+ * latency included), ms3[1] passes queued back to back, ms3[2] one CUDA graph of the pass replayed. */
+int bs_profile_span(bs_handle* h, int dnn, int from, int to, int batch, int reps, double* ms3);
 /* opts: {"batches": [...], "reps": r, "flush_l2": bool} -> reference-schema profile JSON */
 int bs_profile_table(bs_handle* h, const char* opts_json, char** out_json);
 

@@ -471,6 +471,38 @@ int main(int argc, char** argv) {
                     {"mean_completion_s", bits(curve.points[r].metrics.mean_completion / 1000.0)}}
                    .dump()
             << '\n';
+    } else if (kind == "bench") {
+      // bench.py --impl reference: the reference's run_sim (simulator.hpp:
+      // 787-792) on the measured B200 table, one line per (rate, seed) run:
+      // its outcome summary, its served req/s in simulated time (completed /
+      // (last completion - first arrival), the formula bench.py uses for the
+      // live server) and the host wall time of the run.
+      for (const auto& r : job.at("runs")) {
+        json one = job;
+        one["workload"]["rate"] = r.at("rate");
+        one["workload"]["seed"] = r.at("seed");
+        SimJob sj = sim_job_from(one);
+        const auto t0 = std::chrono::steady_clock::now();
+        const SimResult res = run_sim(sj.spec, sj.ps, sj.config, sj.trace ? &*sj.trace : nullptr,
+                                      sj.client ? &*sj.client : nullptr);
+        const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        double first = res.outcomes.empty() ? 0.0 : res.outcomes.front().arrival, last = 0;
+        for (const auto& o : res.outcomes) {
+          first = std::min(first, o.arrival);
+          if (!o.dropped) last = std::max(last, o.completion);
+        }
+        const auto& m = res.metrics;
+        const double span = last - first;
+        out << json{{"rate", r.at("rate")}, {"seed", r.at("seed")}, {"generated", m.generated},
+                    {"completed", m.completed}, {"dropped", m.dropped}, {"on_time", m.on_time},
+                    {"on_time_ratio", m.on_time_ratio}, {"mean_completion_ms", m.mean_completion},
+                    {"p95_completion_ms", m.p95_completion}, {"span_ms", span},
+                    {"served_rps", span > 0 ? m.completed / (span / 1000.0) : 0.0},
+                    {"schedules_computed", m.schedules_computed}, {"mean_solve_wall_ms", m.mean_solve_wall_ms},
+                    {"wall_ms", wall}}
+                   .dump()
+            << '\n';
+      }
     } else if (kind == "random") {
       run_random_job(job, out);
     } else if (kind == "calls") {

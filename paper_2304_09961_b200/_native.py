@@ -1,8 +1,9 @@
-"""ctypes bindings of the two in-tree native libraries.
+"""ctypes bindings of the in-tree native libraries.
 
 libbs_exec.so is the product path (kernels + executor); it is required and
 its absence is an error, never a fallback. libbs_host.so is the CPU-only
-scheduler library (usable without a GPU).
+scheduler library and libbs_nets.so the CPU-only network definitions
+(both usable without a GPU).
 """
 from __future__ import annotations
 
@@ -25,6 +26,7 @@ class bs_conv_desc(C.Structure):
 
 _exec = None
 _host = None
+_nets = None
 
 FP = C.POINTER(C.c_float)
 
@@ -47,6 +49,34 @@ def exec_lib() -> C.CDLL:
         _declare_exec(lib)
         _exec = lib
     return _exec
+
+
+def nets_lib() -> C.CDLL:
+    """Load libbs_nets.so: network definitions, weights and images on the
+    host (no CUDA; the oracles and bench.py's reference arm use it)."""
+    global _nets
+    if _nets is None:
+        path = LIB_DIR / "libbs_nets.so"
+        if not path.exists():
+            raise BsError(f"{path} missing: run __graft_entry__.build()")
+        lib = C.CDLL(str(path))
+        lib.bs_nets_last_error.restype = C.c_char_p
+        lib.bs_describe_suite.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.bs_suite_weights_host.argtypes = [C.c_char_p, FP, C.c_size_t]
+        lib.bs_make_image.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, FP]
+        lib.bs_nets_free.argtypes = [C.c_void_p]
+        lib.bs_nets_free.restype = None
+        _nets = lib
+    return _nets
+
+
+def nets_check(rc: int) -> None:
+    if rc != 0:
+        msg = nets_lib().bs_nets_last_error()
+        text = msg.decode() if msg else ""
+        if rc == -1:
+            raise ValueError(text)
+        raise BsError(f"status {rc}: {text}")
 
 
 def host_lib() -> C.CDLL:

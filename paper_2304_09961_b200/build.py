@@ -1,6 +1,7 @@
 """In-tree build of the native libraries (nvcc / g++ directly, no setuptools).
 
   lib/libbs_host.so  C++20 host scheduler + event loop (no CUDA)
+  lib/libbs_nets.so  network definitions, calibrated weights, synthetic images (no CUDA)
   lib/libbs_exec.so  sm_100a kernels + executor + arena + C-ABI (links host objects)
   bin/batchsim_b200  CLI: simulate / sweep-capacity / validate-profile / oracle-check
 
@@ -110,6 +111,11 @@ def build(verbose: bool = False) -> dict[str, Path]:
         cli = BIN / "batchsim_b200"
         _run(["g++", "-o", str(cli), *map(str, cli_objs), *map(str, host_objs)])
         out["cli"] = cli
+    # CPU-only network definitions + calibrated weights (include/bs_nets.h).
+    nets_objs = [o for o in exec_objs if o.name in ("exec__netdef.cpp.o", "exec__calib.cpp.o", "exec__capi_nets.cpp.o")]
+    nets_so = LIB / "libbs_nets.so"
+    _run(["g++", "-shared", "-o", str(nets_so), *map(str, nets_objs), "-lpthread"])
+    out["nets"] = nets_so
     exec_so = LIB / "libbs_exec.so"
     _run([NVCC, "-shared", *GENCODE, "-o", str(exec_so), *map(str, exec_objs),
           *map(str, host_objs), "-lcudart"])

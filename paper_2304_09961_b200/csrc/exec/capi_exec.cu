@@ -14,6 +14,7 @@
 #include "executor.hpp"
 #include "image.hpp"
 #include "live.hpp"
+#include "nets_json.hpp"
 
 using json = nlohmann::json;
 using namespace bs200;
@@ -44,40 +45,6 @@ int guarded(F&& f) {
     const std::string w = e.what();
     return bs_fail(w.find("full") != std::string::npos ? BS_ENOMEM : BS_ECUDA, w);
   }
-}
-
-json suite_json(const Suite& s, std::size_t blob_floats) {
-  json nets = json::array();
-  for (const NetDef& n : s.nets) {
-    json tensors = json::array();
-    for (const TensorDef& t : n.tensors)
-      tensors.push_back({{"name", t.name}, {"H", t.H}, {"W", t.W}, {"C", t.C}, {"off", t.off}});
-    json ops = json::array();
-    for (const OpDef& o : n.ops) {
-      const char* kind = o.kind == OpKind::conv      ? "conv"
-                         : o.kind == OpKind::maxpool ? "maxpool"
-                         : o.kind == OpKind::avgpool ? "avgpool"
-                         : o.kind == OpKind::dwconv  ? "dwconv"
-                                                     : "softmax";
-      auto ref = [](const TRef& r) { return json::array({r.t, r.coff, r.C}); };
-      ops.push_back({{"kind", kind}, {"name", o.name}, {"in", ref(o.in)}, {"out", ref(o.out)}, {"res", ref(o.res)},
-                     {"k", o.KH}, {"stride", o.stride}, {"pad", o.pad}, {"relu", o.relu},
-                     {"round_out", o.round_out}, {"ceil", o.ceil_mode}, {"Kpad", o.Kpad}, {"w_off", o.w_off},
-                     {"b_off", o.b_off}, {"Ho", o.Ho}, {"Wo", o.Wo}, {"flops", o.flops_per_image},
-                     {"weight_floats", o.weight_floats}});
-    }
-    json layers = json::array();
-    for (const LayerDef& l : n.layers)
-      layers.push_back({{"name", l.name}, {"ops", l.ops}, {"component", l.component}, {"offset", l.offset}});
-    nets.push_back({{"name", n.name}, {"components", n.components}, {"tensors", tensors}, {"ops", ops},
-                    {"layers", layers}, {"input", n.input_t}, {"logits", n.logits_t}, {"probs", n.probs_t},
-                    {"in_H", n.in_H}, {"in_W", n.in_W}, {"in_C", n.in_C}, {"classes", n.num_classes},
-                    {"blob_floats", n.blob_floats}});
-  }
-  json comps = json::array();
-  for (const ComponentDef& c : s.components) comps.push_back({{"id", c.id}, {"num_layers", c.num_layers}});
-  return {{"suite", s.name}, {"components", comps}, {"nets", nets}, {"weights", s.weights.size()},
-          {"slot_floats", blob_floats}, {"max_batch", s.max_batch}};
 }
 
 // Virtual-time serving (the reference's event loop, bit-exact schedules)
@@ -170,37 +137,11 @@ int bs_suite_json(bs_handle* h, char** out) {
   });
 }
 
-int bs_describe_suite(const char* suite, char** out) {
-  return guarded([&] {
-    const Suite s = build_suite(suite);
-    std::size_t slot = 0;
-    for (const NetDef& n : s.nets) slot = std::max<std::size_t>(slot, static_cast<std::size_t>(n.blob_floats));
-    *out = dup_str(suite_json(s, slot).dump());
-    return BS_OK;
-  });
-}
-
-int bs_suite_weights_host(const char* suite, float* dst, size_t n) {
-  return guarded([&] {
-    const Suite s = build_suite(suite);
-    if (n < s.weights.size()) throw std::invalid_argument("bs_suite_weights_host: buffer too small");
-    std::memcpy(dst, s.weights.data(), s.weights.size() * sizeof(float));
-    return BS_OK;
-  });
-}
-
 int bs_read_weights(bs_handle* h, float* dst, size_t n) {
   return guarded([&] {
     const auto& w = h->ex->suite().weights;
     if (n < w.size()) throw std::invalid_argument("bs_read_weights: buffer too small");
     std::memcpy(dst, w.data(), w.size() * sizeof(float));
-    return BS_OK;
-  });
-}
-
-int bs_make_image(uint64_t seed, uint64_t index, int H, int W, int C, int real_c, float* out) {
-  return guarded([&] {
-    synth_image(seed, index, H, W, C, real_c, out);
     return BS_OK;
   });
 }
@@ -283,6 +224,13 @@ int bs_sync(bs_handle* h) {
 int bs_profile_layer(bs_handle* h, int dnn, int layer, int batch, int reps, int flush_l2, double* ms) {
   return guarded([&] {
     *ms = h->ex->profile_layer(dnn, layer, batch, reps, flush_l2 != 0);
+    return BS_OK;
+  });
+}
+
+int bs_profile_span(bs_handle* h, int dnn, int from, int to, int batch, int reps, double* ms3) {
+  return guarded([&] {
+    h->ex->profile_span(dnn, from, to, batch, reps, ms3);
     return BS_OK;
   });
 }

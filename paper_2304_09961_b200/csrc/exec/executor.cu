@@ -894,6 +894,53 @@ double Executor::profile_layer(int dnn, int layer, int batch, int reps, bool flu
   return ms[ms.size() / 2];
 }
 
+void Executor::profile_span(int dnn, int from, int to, int batch, int reps, double out[3]) {
+  if (batch < 1 || batch > max_batch_) throw std::invalid_argument("profile batch out of range");
+  cudaEvent_t a, b;
+  ck(cudaEventCreate(&a), "ev");
+  ck(cudaEventCreate(&b), "ev");
+  auto pass = [&] {
+    for (int k = from; k <= to; ++k) run_layer(dnn, k, scratch_ptrs_, batch);
+  };
+  auto elapsed = [&] {
+    float t = 0;
+    ck(cudaEventSynchronize(b), "ev sync");
+    ck(cudaEventElapsedTime(&t, a, b), "elapsed");
+    return static_cast<double>(t);
+  };
+  pass();
+  sync();
+  std::vector<double> v;
+  for (int r = 0; r < reps; ++r) {
+    ck(cudaEventRecord(a, stream_), "ev");
+    pass();
+    ck(cudaEventRecord(b, stream_), "ev");
+    v.push_back(elapsed());
+  }
+  std::sort(v.begin(), v.end());
+  out[0] = v[v.size() / 2];
+  ck(cudaEventRecord(a, stream_), "ev");
+  for (int r = 0; r < reps; ++r) pass();
+  ck(cudaEventRecord(b, stream_), "ev");
+  out[1] = elapsed() / reps;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+  pass();
+  ck(cudaStreamEndCapture(stream_, &g), "end capture");
+  ck(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+  ck(cudaGraphLaunch(ge, stream_), "graph launch");
+  sync();
+  ck(cudaEventRecord(a, stream_), "ev");
+  for (int r = 0; r < reps; ++r) ck(cudaGraphLaunch(ge, stream_), "graph launch");
+  ck(cudaEventRecord(b, stream_), "ev");
+  out[2] = elapsed() / reps;
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+}
+
 // ------------------------------------------------------------- image pools
 
 void Executor::make_image_pool(int dnn, int count, std::uint64_t seed) {

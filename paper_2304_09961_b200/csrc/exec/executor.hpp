@@ -84,6 +84,10 @@ class Executor {
   // Median of `reps` CUDA-event timings of one layer at batch b (cold L2 if
   // flush), on scratch blobs.
   double profile_layer(int dnn, int layer, int batch, int reps, bool flush_l2);
+  // Layers [from, to] at one batch on scratch blobs, per pass (ms):
+  // out[0] = synchronised per pass (launch latency included), out[1] = reps
+  // passes queued back to back, out[2] = one CUDA graph of the pass replayed.
+  void profile_span(int dnn, int from, int to, int batch, int reps, double out[3]);
   // Sampled launch timing: every `every`-th conv launch (and every other
   // kernel) gets an event pair from a preallocated pool.
   void enable_stats(bool on, int every = 1);

@@ -210,6 +210,7 @@ json serve_live(Executor& ex, const json& j) {
         ex.step(plan_no, st.segment, dnn_map[static_cast<std::size_t>(seg.dnn)], st.layer_from, st.layer_to, members,
                 seg.riders);
         ++n_steps;
+        step_batch_hist.push_back(static_cast<int>(members.size() + seg.riders.size()));
         // Effects apply at launch (the stream guarantees completion order);
         // completion times are stamped when the step's event fires.
         InFlight f;
@@ -341,6 +342,18 @@ json serve_live(Executor& ex, const json& j) {
   out["sched_ms_total"] = sched_ms;
   out["sched_ms_max"] = max_sched_ms;
   out["launches"] = ex.launches() - launches0;
+  {
+    // step size distribution (members + riders of each launched step)
+    double sum = 0;
+    json hist = json::object();
+    for (int b : step_batch_hist) {
+      sum += b;
+      const int bucket = b <= 1 ? 1 : b <= 4 ? 4 : b <= 16 ? 16 : b <= 48 ? 48 : 90;
+      hist[std::to_string(bucket)] = hist.value(std::to_string(bucket), 0) + 1;
+    }
+    out["step_members_mean"] = step_batch_hist.empty() ? 0.0 : sum / static_cast<double>(step_batch_hist.size());
+    out["step_members_hist"] = hist;
+  }
   out["h2d_bytes"] = h2d_bytes;
   out["d2h_bytes"] = d2h_bytes;
   out["top1"] = top1;

@@ -4,6 +4,8 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 
 #include "bsb/core.hpp"
@@ -106,6 +108,7 @@ class Builder {
     op.stride = stride;
     op.pad = pad;
     op.relu = relu;
+    op.wscale = wscale;
     const TensorDef& ti = T(in.t);
     op.Ho = (ti.H + 2 * pad - k) / stride + 1;
     op.Wo = (ti.W + 2 * pad - k) / stride + 1;
@@ -240,7 +243,7 @@ class Builder {
     batchsim::SplitMix64 g(seed_ ^ fnv1a(key));
     pool.resize(pool.size() + static_cast<std::size_t>(count));
     for (long i = 0; i < count; ++i)
-      pool[static_cast<std::size_t>(op.w_off + i)] = round_tf32_host(value(i, g));
+      pool[static_cast<std::size_t>(op.w_off + i)] = value(i, g);  // TF32-rounded after calibration
     align();
     op.b_off = static_cast<long>(pool.size());
     pool.resize(pool.size() + static_cast<std::size_t>(bias_count));
@@ -512,7 +515,9 @@ void mobilenet_v2(Builder& b) {
 
 }  // namespace
 
-Suite build_suite(const std::string& name, std::uint64_t seed) {
+namespace {
+
+Suite build_suite_uncached(const std::string& name, std::uint64_t seed) {
   Suite s;
   s.name = name;
   auto add = [&](const char* dnn, void (*fn)(Builder&)) {
@@ -572,7 +577,32 @@ Suite build_suite(const std::string& name, std::uint64_t seed) {
       }
     }
   }
+  // Calibrate, then round every weight matrix to TF32 (the
+  // tensor-core operand precision; biases stay fp32).
+  std::set<long> calibrated;
+  for (const NetDef& n : s.nets) calibrate_net(s, n, calibrated);
+  for (const NetDef& n : s.nets)
+    for (const OpDef& op : n.ops) {
+      long count = 0;
+      if (op.kind == OpKind::conv) count = static_cast<long>(op.out.C) * op.Kpad;
+      if (op.kind == OpKind::dwconv) count = 9L * op.in.C;
+      for (long i = 0; i < count; ++i) {
+        float& v = s.weights[static_cast<std::size_t>(op.w_off + i)];
+        v = round_tf32_host(v);
+      }
+    }
   return s;
+}
+
+}  // namespace
+
+Suite build_suite(const std::string& name, std::uint64_t seed) {
+  static std::mutex mu;
+  static std::map<std::pair<std::string, std::uint64_t>, Suite> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({name, seed});
+  if (it == cache.end()) it = cache.emplace(std::make_pair(name, seed), build_suite_uncached(name, seed)).first;
+  return it->second;
 }
 
 double op_bytes(const NetDef& net, const OpDef& op, int batch) {

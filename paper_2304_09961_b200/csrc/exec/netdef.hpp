@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <map>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -48,6 +49,7 @@ struct OpDef {
   int Kpad = 0;                 // conv: padded K (row stride of the weight matrix)
   long w_off = -1, b_off = -1;  // offsets into the executor's weight pool (floats)
   int Ho = 0, Wo = 0;
+  double wscale = 1.0;          // residual-branch gain (calibration target std)
   double flops_per_image = 0;   // algorithmic, 2*MACs
   long weight_floats = 0;
 };
@@ -91,7 +93,14 @@ struct Suite {
 // Known suites: "small_cnn", "googlenet", "resnet50", "mobilenet_v2",
 // "resnet50_pair" (shared backbone + two heads), "hetero3" (GoogLeNet +
 // ResNet-50 + MobileNetV2), "collab" (GoogLeNet + ResNet-50).
+// Weights are He-normal draws calibrated on a fixed batch (calib.cpp: BN
+// folded with calibration statistics, classifier centred), then TF32-rounded.
+// Built once per (name, seed) per process and copied out.
 Suite build_suite(const std::string& name, std::uint64_t seed = 2304099610ULL);
+
+// calib.cpp: calibrates the ops of `net` whose weights are not yet in
+// `calibrated` (keyed by w_off), in forward order.
+void calibrate_net(Suite& s, const NetDef& net, std::set<long>& calibrated);
 
 // Bytes an op moves at batch b (weights once + activations per image) and
 // its FLOPs: the algorithmic numerator of the roofline.

@@ -13,7 +13,7 @@ import json
 
 import numpy as np
 
-from ._native import BsError, FP, exec_lib
+from ._native import BsError, FP, exec_lib, nets_check, nets_lib
 
 _declared = False
 
@@ -37,7 +37,6 @@ def _lib():
             "bs_destroy": ([H], C.c_int),
             "bs_suite_json": ([H, C.POINTER(C.c_void_p)], C.c_int),
             "bs_read_weights": ([H, FP, C.c_size_t], C.c_int),
-            "bs_make_image": ([C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, FP], C.c_int),
             "bs_admit": ([H, C.c_int64, C.c_int, C.c_int, FP], C.c_int),
             "bs_plan": ([H, C.c_int], C.c_int),
             "bs_step": ([H, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(bs_member), C.c_int,
@@ -48,11 +47,11 @@ def _lib():
             "bs_read_blob": ([H, C.c_int64, FP, C.c_size_t], C.c_int),
             "bs_sync": ([H], C.c_int),
             "bs_profile_layer": ([H, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
+            "bs_profile_span": ([H, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
             "bs_profile_table": ([H, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
             "bs_replay": ([H, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
             "bs_serve": ([H, C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
             "bs_free": ([C.c_void_p], None),
-            "bs_describe_suite": ([C.c_char_p, C.POINTER(C.c_void_p)], C.c_int),
             "bs_set_precision": ([H, C.c_char_p], C.c_int),
             "bs_stats": ([H, C.c_int, C.c_int], C.c_int),
             "bs_stats_summary": ([H, C.c_double, C.c_double, C.POINTER(C.c_void_p)], C.c_int),
@@ -84,15 +83,27 @@ def _take_string(ptr: C.c_void_p) -> str:
 
 
 def describe_suite(suite: str) -> dict:
-    """Network description of a suite, built on the host (no GPU needed)."""
+    """Network description of a suite, built on the host (libbs_nets.so, no GPU needed)."""
+    lib = nets_lib()
     out = C.c_void_p()
-    _check(_lib().bs_describe_suite(suite.encode(), C.byref(out)))
-    return json.loads(_take_string(out))
+    nets_check(lib.bs_describe_suite(suite.encode(), C.byref(out)))
+    try:
+        return json.loads(C.string_at(out).decode())
+    finally:
+        lib.bs_nets_free(out)
+
+
+def suite_weights(suite: str, desc: dict | None = None) -> np.ndarray:
+    """The suite's calibrated weight pool, built on the host (libbs_nets.so)."""
+    desc = desc or describe_suite(suite)
+    w = np.empty(desc["weights"], np.float32)
+    nets_check(nets_lib().bs_suite_weights_host(suite.encode(), w.ctypes.data_as(FP), w.size))
+    return w
 
 
 def make_image(seed: int, index: int, H: int, W: int, C_: int, real_c: int = 3) -> np.ndarray:
     out = np.empty((H, W, C_), np.float32)
-    _check(_lib().bs_make_image(seed, index, H, W, C_, real_c, out.ctypes.data_as(FP)))
+    nets_check(nets_lib().bs_make_image(seed, index, H, W, C_, real_c, out.ctypes.data_as(FP)))
     return out
 
 
@@ -193,6 +204,12 @@ class Executor:
         opts = json.dumps({"batches": list(batches), "reps": reps, "flush_l2": flush_l2, "tune_tiles": tune_tiles})
         _check(_lib().bs_profile_table(self._h, opts.encode(), C.byref(out)))
         return json.loads(_take_string(out))
+
+    def profile_span(self, dnn: int, lo: int, hi: int, batch: int, reps: int = 20) -> tuple[float, float, float]:
+        """ms per pass of layers [lo, hi] at `batch`: (synchronised, back to back, CUDA graph)."""
+        out = (C.c_double * 3)()
+        _check(_lib().bs_profile_span(self._h, dnn, lo, hi, batch, reps, out))
+        return out[0], out[1], out[2]
 
     def stats(self, enable: bool, every: int = 1):
         _check(_lib().bs_stats(self._h, int(enable), every))

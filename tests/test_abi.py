@@ -15,7 +15,8 @@ def declared(header: str) -> list[str]:
     return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+[\s\*]+(bs_\w+)\s*\(", text, flags=re.M)))
 
 
-@pytest.mark.parametrize("header,lib", [("bs_exec.h", "libbs_exec.so"), ("bs_host.h", "libbs_host.so")])
+@pytest.mark.parametrize("header,lib", [("bs_exec.h", "libbs_exec.so"), ("bs_host.h", "libbs_host.so"),
+                                        ("bs_nets.h", "libbs_nets.so")])
 def test_library_exports_header(header, lib):
     names = declared(header)
     assert len(names) >= 3

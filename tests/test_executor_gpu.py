@@ -8,7 +8,7 @@ the same 1e-3 bound on every tensor the layer wrote.
 import numpy as np
 import pytest
 
-from oracle.forward import NetOracle, rel_err
+from oracle.forward import NetOracle, assert_request_matches, rel_err
 
 TOL = 1e-3
 pytestmark = pytest.mark.gpu
@@ -66,10 +66,9 @@ def test_googlenet_ragged_steps_match_oracle(googlenet):
         p_ref = orc.probs(blob)
         l_ref = orc.logits(blob)
         logits = ex.read_blob(i)[orc.d["tensors"][orc.d["logits"]]["off"]:][:1000]
-        assert rel_err(logits, l_ref) < TOL
+        assert_request_matches(logits, l_ref, TOL)
         p = ex.retire(i, 1000)
-        assert rel_err(p, p_ref) < TOL
-        assert int(np.argmax(p)) == int(np.argmax(p_ref))
+        assert_request_matches(p, p_ref, TOL)
 
 
 def test_googlenet_full_batch_90(googlenet):
@@ -77,16 +76,15 @@ def test_googlenet_full_batch_90(googlenet):
     orc = NetOracle(ex.desc, 0, w)
     ids = list(range(100, 190))
     for i in ids:
-        ex.admit(i, 0, image_for(ex, 0, i % 7))
+        ex.admit(i, 0, image_for(ex, 0, i))
     ex.plan(2)
     ex.step(2, 0, 0, 1, 22, [(i, 1) for i in ids])
     probs = {i: ex.retire(i, 1000) for i in ids}
-    for j in range(3):  # spot-check distinct images
-        ref = orc.probs(orc.forward(image_for(ex, 0, j)))
-        for i in ids:
-            if i % 7 == j:
-                assert rel_err(probs[i], ref) < TOL
-                assert int(np.argmax(probs[i])) == int(np.argmax(ref))
+    # non-degenerate outputs: 90 distinct inputs give many distinct classes
+    assert len({int(np.argmax(p)) for p in probs.values()}) >= 30
+    for i in ids[:6]:  # oracle check on a sample of distinct images
+        ref = orc.probs(orc.forward(image_for(ex, 0, i)))
+        assert_request_matches(probs[i], ref, TOL)
 
 
 def test_small_cnn_replay_config1():
@@ -108,8 +106,8 @@ def test_small_cnn_replay_config1():
         for i in range(1, 41):
             ref = orc.probs(orc.forward(image_for(ex, 0, i - 1, seed=7)))
             got = np.array(res["probs"][str(i)], np.float32)[:10]
-            assert rel_err(got, ref) < TOL
-            assert res["top1"][i - 1] == int(np.argmax(ref))
+            assert_request_matches(got, ref, TOL)
+            assert res["top1"][i - 1] == int(np.argmax(got))
 
 
 def test_resnet50_pair_riders_and_rewind():
@@ -138,8 +136,8 @@ def test_resnet50_pair_riders_and_rewind():
         pa, pb = ex.retire(1, 1000), ex.retire(2, 365)
         ra = oa.probs(oa.forward(ia))
         rb = ob.probs(ob.forward(ib))
-        assert rel_err(pa, ra) < TOL and int(np.argmax(pa)) == int(np.argmax(ra))
-        assert rel_err(pb, rb) < TOL and int(np.argmax(pb)) == int(np.argmax(rb))
+        assert_request_matches(pa, ra, TOL)
+        assert_request_matches(pb, rb, TOL)
 
 
 def test_mobilenet_v2_matches_oracle():
@@ -156,7 +154,7 @@ def test_mobilenet_v2_matches_oracle():
         for i, img in enumerate(imgs):
             p = ex.retire(i + 1, 1000)
             ref = orc.probs(orc.forward(img))
-            assert rel_err(p, ref) < TOL and int(np.argmax(p)) == int(np.argmax(ref))
+            assert_request_matches(p, ref, TOL)
 
 
 def test_profile_table_schema_loads_in_scheduler():
@@ -200,8 +198,8 @@ def _check_replay_outputs(ex, out, image_seed, orcs, per_dnn=3):
         orc = orcs[dnn]
         ref = orc.probs(orc.forward(image_for(ex, dnn, rid - 1, seed=image_seed)))
         got = np.array(res["probs"][str(rid)], np.float32)[:ref.size]
-        assert rel_err(got, ref) < TOL, (rid, dnn)
-        assert int(np.argmax(got)) == int(np.argmax(ref)) == res["top1"][rid - 1]
+        assert_request_matches(got, ref, TOL)
+        assert int(np.argmax(got)) == res["top1"][rid - 1], (rid, dnn)
         checked += 1
     return seen, checked
 
@@ -287,8 +285,7 @@ def test_grouped_conv_launches_match_ungrouped(monkeypatch):
     assert launches["1"] < launches["0"]
     for i in ids:
         assert rel_err(probs["1"][i], probs["0"][i]) < 1e-5
-        assert rel_err(probs["1"][i], refs[i % 5]) < TOL
-        assert int(np.argmax(probs["1"][i])) == int(np.argmax(refs[i % 5]))
+        assert_request_matches(probs["1"][i], refs[i % 5], TOL)
 
 
 def test_tile_autotune_keeps_parity():
@@ -310,4 +307,4 @@ def test_tile_autotune_keeps_parity():
         refs = {j: orc.probs(orc.forward(image_for(ex, 0, j))) for j in range(3)}
         for i in ids:
             p = ex.retire(i, 1000)
-            assert rel_err(p, refs[i % 3]) < TOL and int(np.argmax(p)) == int(np.argmax(refs[i % 3]))
+            assert_request_matches(p, refs[i % 3], TOL)
