@@ -382,7 +382,10 @@ def ncu_traffic():
 
 
 REF_DUMP = ROOT / "oracle" / "_ref" / "ref_dump"
-TABLES = {2: ROOT / "profiles" / "r02" / "googlenet_table_b200.json"}
+TABLES = {1: ROOT / "profiles" / "r02" / "small_cnn_table_b200.json",
+          2: ROOT / "profiles" / "r02" / "googlenet_table_b200.json",
+          3: ROOT / "profiles" / "r02" / "resnet50_pair_table_b200.json",
+          4: ROOT / "profiles" / "r02" / "hetero3_table_b200.json"}
 
 
 def cpu_model() -> str:

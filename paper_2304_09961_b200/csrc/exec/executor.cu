@@ -85,15 +85,6 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   ck(cudaMemcpy(scratch_ptrs_, hp.data(), hp.size() * sizeof(float*), cudaMemcpyHostToDevice), "scratch ptrs H2D");
   pool_.assign(suite_.nets.size(), nullptr);
   pool_n_.assign(suite_.nets.size(), 0);
-  // Split-K workspaces: one per stream that launches convs (serving stream,
-  // client-prefix side stream), so concurrent launches never share counters.
-  for (ConvWorkspace* w : {&conv_ws_, &side_ws_}) {
-    w->partial_floats = conv_workspace_floats();
-    w->n_counters = conv_workspace_counters();
-    ck(cudaMalloc(&w->partials, w->partial_floats * sizeof(float)), "split-K workspace");
-    ck(cudaMalloc(&w->counters, w->n_counters * sizeof(int)), "split-K counters");
-    ck(cudaMemset(w->counters, 0, w->n_counters * sizeof(int)), "split-K counters zero");
-  }
   // One TMA descriptor per conv/FC weight matrix (weights never move).
   wmaps_.resize(suite_.nets.size());
   wmaps_wide_.resize(suite_.nets.size());
@@ -306,10 +297,6 @@ Executor::~Executor() {
   cudaFree(staging_);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (float* p : pool_) cudaFree(p);
-  for (ConvWorkspace* w : {&conv_ws_, &side_ws_}) {
-    cudaFree(w->partials);
-    cudaFree(w->counters);
-  }
   cudaFree(d_weights_);
   cudaFree(d_win_weights_);
   cudaFree(d_tap_weights_);
@@ -393,22 +380,16 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
   {
     const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
     const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
+    ConvChoice c{};
     if (static_cast<int>(ni) == tune_net_ && static_cast<int>(oi) == tune_op_) {
-      p.wide_pref = tune_pref_;
-    } else if (!tune_batches_.empty() && ni < wide_pref_.size() && oi < wide_pref_[ni].size() &&
-               !wide_pref_[ni][oi].empty()) {
-      // nearest tuned batch (by ratio)
-      std::size_t best = 0;
-      double bd = 1e30;
-      for (std::size_t t = 0; t < tune_batches_.size(); ++t) {
-        const double d = std::fabs(std::log(static_cast<double>(tune_batches_[t]) / batch));
-        if (d < bd) {
-          bd = d;
-          best = t;
-        }
-      }
-      p.wide_pref = wide_pref_[ni][oi][best];
+      c = tune_choice_;
+    } else {
+      const int t = tuned_index(batch);
+      if (t >= 0 && ni < conv_pref_.size() && oi < conv_pref_[ni].size() && !conv_pref_[ni][oi].empty())
+        c = conv_pref_[ni][oi][static_cast<std::size_t>(t)];
     }
+    p.wide_pref = c.wide;
+    p.ks_force = c.ks;
   }
   {
     const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
@@ -429,8 +410,26 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
   return p;
 }
 
-void Executor::launch_group(const NetDef& net, const OpDef& a, const OpDef& b, float* const* d_ptrs, int batch) {
+void Executor::launch_group(const NetDef& net, int layer, int item, const OpDef& a, const OpDef& b,
+                            float* const* d_ptrs, int batch) {
   const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
+  // Grouped or separate: the tuning override, else the tuned choice of the
+  // nearest batch, else the launcher's rule (declines for split / wide).
+  int pref = 0;
+  if (static_cast<int>(ni) == tune_net_ && layer == tune_layer_ && item == tune_item_) {
+    pref = tune_group_;
+  } else {
+    const int t = tuned_index(batch);
+    if (t >= 0 && ni < group_pref_.size()) {
+      const auto& g = group_pref_[ni][static_cast<std::size_t>(layer - 1)][static_cast<std::size_t>(item)];
+      if (!g.empty()) pref = g[static_cast<std::size_t>(t)];
+    }
+  }
+  if (pref < 0) {
+    launch_op(net, a, d_ptrs, batch);
+    launch_op(net, b, d_ptrs, batch);
+    return;
+  }
   ConvParams pa = conv_params(net, a, d_ptrs, batch), pb = conv_params(net, b, d_ptrs, batch);
   const std::size_t ia = static_cast<std::size_t>(&a - net.ops.data()), ib = static_cast<std::size_t>(&b - net.ops.data());
   if (gmap_ok_[ni][ia]) pa.wmap = gmaps_[ni][ia];
@@ -446,7 +445,7 @@ void Executor::launch_group(const NetDef& net, const OpDef& a, const OpDef& b, f
     st.t1 = event_pool_[ev_next_++];
     ck(cudaEventRecord(st.t0, stream_), "ev rec");
   }
-  const cudaError_t e = launch_conv_tc_group(pa, pb, *ws_, stream_);
+  const cudaError_t e = launch_conv_tc_group(pa, pb, stream_, pref > 0, std::max(1, pref));
   if (e == cudaErrorNotSupported) {  // split-K / wide tiles win at this batch
     if (sample) {
       ev_next_ -= 2;
@@ -484,7 +483,7 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
   cudaError_t e = cudaSuccess;
   switch (op.kind) {
     case OpKind::conv: {
-      e = launch_conv_tc(conv_params(net, op, d_ptrs, batch), *ws_, stream_);
+      e = launch_conv_tc(conv_params(net, op, d_ptrs, batch), stream_);
       break;
     }
     case OpKind::maxpool: {
@@ -522,9 +521,13 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
 void Executor::run_layer(int dnn, int layer, float* const* d_ptrs, int batch) {
   if (batch <= 0) return;
   const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
-  for (const LayerItem& it : plans_[static_cast<std::size_t>(dnn)][static_cast<std::size_t>(layer - 1)]) {
+  const auto& items = plans_[static_cast<std::size_t>(dnn)][static_cast<std::size_t>(layer - 1)];
+  for (std::size_t i = 0; i < items.size(); ++i) {
+    const LayerItem& it = items[i];
     if (it.b < 0) launch_op(net, net.ops[static_cast<std::size_t>(it.a)], d_ptrs, batch);
-    else launch_group(net, net.ops[static_cast<std::size_t>(it.a)], net.ops[static_cast<std::size_t>(it.b)], d_ptrs, batch);
+    else
+      launch_group(net, layer, static_cast<int>(i), net.ops[static_cast<std::size_t>(it.a)],
+                   net.ops[static_cast<std::size_t>(it.b)], d_ptrs, batch);
   }
 }
 
@@ -563,16 +566,13 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
     host[0] = s.blob;
     ck(cudaMemcpyAsync(d, host, sizeof(float*), cudaMemcpyHostToDevice, side_), "table H2D");
     std::swap(stream_, side_);
-    ws_ = &side_ws_;
     try {
       for (int k = 1; k < entry_layer; ++k) run_layer(dnn, k, d, 1);
     } catch (...) {
       std::swap(stream_, side_);
-      ws_ = &conv_ws_;
       throw;
     }
     std::swap(stream_, side_);
-    ws_ = &conv_ws_;
     ck(cudaEventRecord(mine.done, side_), "chunk done");
     mine.in_use = true;
     s.ready = next_ready_event();
@@ -828,41 +828,110 @@ void Executor::clear_stats() {
   ev_next_ = 0;
 }
 
+int Executor::tuned_index(int batch) const {
+  if (tune_batches_.empty()) return -1;
+  // nearest tuned batch by ratio
+  std::size_t best = 0;
+  double bd = 1e30;
+  for (std::size_t t = 0; t < tune_batches_.size(); ++t) {
+    const double d = std::fabs(std::log(static_cast<double>(tune_batches_[t]) / batch));
+    if (d < bd) {
+      bd = d;
+      best = t;
+    }
+  }
+  return static_cast<int>(best);
+}
+
 std::string Executor::tune_tiles(const std::vector<int>& batches, int reps) {
   tune_batches_.clear();
-  wide_pref_.assign(suite_.nets.size(), {});
+  conv_pref_.assign(suite_.nets.size(), {});
+  group_pref_.assign(suite_.nets.size(), {});
   std::vector<int> bs;
   for (int b : batches)
     if (b >= 1 && b <= max_batch_) bs.push_back(b);
   std::sort(bs.begin(), bs.end());
+  bs.erase(std::unique(bs.begin(), bs.end()), bs.end());
+  // Choices apply as soon as they are made (an untuned entry is the
+  // launcher's rule), so a pair's "separate" timing uses its tuned convs.
+  tune_batches_ = bs;
   std::string log = "[";
+  auto note = [&](const std::string& what, int b, const char* choice, double ms) {
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "%s[\"%s\",%d,\"%s\",%.4f]", log.size() > 1 ? "," : "", what.c_str(), b, choice, ms);
+    log += buf;
+  };
   for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
     const NetDef& net = suite_.nets[n];
-    wide_pref_[n].assign(net.ops.size(), {});
+    conv_pref_[n].assign(net.ops.size(), std::vector<ConvChoice>(bs.size()));
+    group_pref_[n].resize(plans_[n].size());
+    for (std::size_t k = 0; k < plans_[n].size(); ++k)
+      group_pref_[n][k].assign(plans_[n][k].size(), std::vector<signed char>(bs.size(), 0));
     for (int k = 1; k <= net.num_layers(); ++k) {
-      for (int oi : net.layers[static_cast<std::size_t>(k - 1)].ops) {
-        const OpDef& op = net.ops[static_cast<std::size_t>(oi)];
-        if (op.kind != OpKind::conv || op.out.C <= 128) continue;
-        auto& prefs = wide_pref_[n][static_cast<std::size_t>(oi)];
-        prefs.assign(bs.size(), 0);
-        for (std::size_t t = 0; t < bs.size(); ++t) {
+      const auto& items = plans_[n][static_cast<std::size_t>(k - 1)];
+      for (std::size_t t = 0; t < bs.size(); ++t) {
+        const int b = bs[t];
+        auto time_layer = [&] { return profile_layer(static_cast<int>(n), k, b, reps, false); };
+        for (std::size_t ii = 0; ii < items.size(); ++ii) {
+          const LayerItem& it = items[ii];
+          const bool pair = it.b >= 0;
           tune_net_ = static_cast<int>(n);
-          tune_op_ = oi;
-          tune_pref_ = 1;
-          const double tw = profile_layer(static_cast<int>(n), k, bs[t], reps, false);
-          tune_pref_ = 2;
-          const double tn = profile_layer(static_cast<int>(n), k, bs[t], reps, false);
-          tune_net_ = tune_op_ = -1;
-          prefs[t] = tw < 0.97 * tn ? 1 : 2;  // wide only on a clear win
-          char buf[160];
-          std::snprintf(buf, sizeof buf, "%s[\"%s\",%d,%.4f,%.4f]", log.size() > 1 ? "," : "", op.name.c_str(), bs[t],
-                        tw, tn);
-          log += buf;
+          if (pair) {  // tune the two convs as separate launches first
+            tune_layer_ = k;
+            tune_item_ = static_cast<int>(ii);
+            tune_group_ = -1;
+          }
+          for (int oi : {it.a, it.b}) {
+            if (oi < 0) continue;
+            const OpDef& op = net.ops[static_cast<std::size_t>(oi)];
+            if (op.kind != OpKind::conv) continue;
+            // candidates: the launcher's own choice first, then forced splits
+            // (narrow tiles), then 128 x 256 tiles unsplit (N > 128)
+            std::vector<ConvChoice> cands{{0, 0}};
+            for (signed char ks : {1, 2, 4, 8}) cands.push_back({2, ks});
+            if (op.out.C > 128) cands.push_back({1, 1});
+            tune_op_ = oi;
+            ConvChoice best{};
+            double best_ms = 1e30;
+            for (const ConvChoice& c : cands) {
+              tune_choice_ = c;
+              const double ms = time_layer();
+              char name[16];
+              std::snprintf(name, sizeof name, "w%d/k%d", c.wide, c.ks);
+              note(op.name, b, name, ms);
+              if (ms < 0.98 * best_ms) {  // switch only on a clear win
+                best_ms = ms;
+                best = c;
+              }
+            }
+            conv_pref_[n][static_cast<std::size_t>(oi)][t] = best;
+            tune_op_ = -1;
+          }
+          if (pair) {
+            const std::string nm =
+                net.ops[static_cast<std::size_t>(it.a)].name + "+" + net.ops[static_cast<std::size_t>(it.b)].name;
+            signed char best_g = -1;
+            double best_ms = time_layer();  // separate, with the tuned convs
+            note(nm, b, "separate", best_ms);
+            for (signed char g : {1, 2, 4, 8}) {
+              tune_group_ = g;
+              const double ms = time_layer();
+              char name[16];
+              std::snprintf(name, sizeof name, "grouped/k%d", g);
+              note(nm, b, name, ms);
+              if (ms < 0.98 * best_ms) {
+                best_ms = ms;
+                best_g = g;
+              }
+            }
+            group_pref_[n][static_cast<std::size_t>(k - 1)][ii][t] = best_g;
+          }
+          tune_net_ = tune_layer_ = tune_item_ = -1;
+          tune_group_ = 0;
         }
       }
     }
   }
-  tune_batches_ = bs;
   return log + "]";
 }
 

@@ -122,20 +122,34 @@ class Executor {
   ConvParams conv_params(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch) const;
   // Two independent convs of one layer in one persistent launch (falls back
   // to two launches when the launcher declines: split-K or wide tiles win).
-  void launch_group(const NetDef& net, const OpDef& a, const OpDef& b, float* const* d_ptrs, int batch);
+  void launch_group(const NetDef& net, int layer, int item, const OpDef& a, const OpDef& b, float* const* d_ptrs,
+                    int batch);
   void plan_groups();
 
  public:
-  // Profile-time autotune of the conv tile width: for every conv with
-  // N > 128 and each batch in `batches`, the layer is timed with that conv on
-  // 128 x 256 and on 128-wide tiles; launches then use the faster width for
-  // the nearest tuned batch. Returns the decisions as JSON text.
+  // Profile-time autotune of the conv launch choices, per conv and per
+  // batch in `batches`: the K split (1 / 2 / 4 / 8 or the launcher's cost
+  // model), 128 x 256 vs 128-wide tiles (N > 128), and for the conv pairs of
+  // grouped launches whether one grouped launch beats two separate ones.
+  // Each candidate is timed on its whole layer; launches then use the
+  // fastest choice of the nearest tuned batch. Returns the timings as JSON.
   std::string tune_tiles(const std::vector<int>& batches, int reps);
 
  private:
-  std::vector<int> tune_batches_;                              // sorted tuned batch sizes
-  std::vector<std::vector<std::vector<signed char>>> wide_pref_;  // [net][op][tuned batch]
-  int tune_net_ = -1, tune_op_ = -1, tune_pref_ = 0;           // override while tuning
+  struct ConvChoice {
+    signed char wide = 0;  // 0 launcher rule, 1 128 x 256, 2 128-wide
+    signed char ks = 0;    // 0 launcher cost model, else forced K split
+  };
+  int tuned_index(int batch) const;                              // nearest tuned batch, -1 if none
+  std::vector<int> tune_batches_;                                // sorted tuned batch sizes
+  std::vector<std::vector<std::vector<ConvChoice>>> conv_pref_;  // [net][op][tuned batch]
+  // [net][layer - 1][item][tuned batch]: 0 launcher rule, -1 separate,
+  // k >= 1 grouped with a k-way K split
+  std::vector<std::vector<std::vector<std::vector<signed char>>>> group_pref_;
+  // overrides while tuning
+  int tune_net_ = -1, tune_op_ = -1;
+  ConvChoice tune_choice_{};
+  int tune_layer_ = -1, tune_item_ = -1, tune_group_ = 0;
 
   Suite suite_;
   int device_ = 0;
@@ -215,9 +229,6 @@ class Executor {
   std::vector<std::vector<char>> gmap_ok_;
   float* d_tap_weights_ = nullptr;                // (kh, kw < 32 / Cin, ci) copies of the stem weights
   long total_slots_ = 0;
-  ConvWorkspace conv_ws_;                         // split-K partials + tile counters (serving stream)
-  ConvWorkspace side_ws_;                         // the same for the client-prefix side stream
-  const ConvWorkspace* ws_ = &conv_ws_;           // workspace of the stream launching now
   bool split_ = true;
   bool stats_on_ = false;
   int stats_every_ = 1;

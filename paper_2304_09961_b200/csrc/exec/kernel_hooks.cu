@@ -27,7 +27,6 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
   float *dwin = nullptr;
   float *din = nullptr, *dw = nullptr, *db = nullptr, *dout = nullptr, *dres = nullptr;
   float** ptrs = nullptr;
-  ConvWorkspace ws;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   int rc = BS_OK;
 #define CK(x)                                           \
@@ -45,11 +44,6 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     if (bias_host) CK(cudaMalloc(&db, d->N * sizeof(float)));
     if (res_host) CK(cudaMalloc(&dres, res_img * nimg * sizeof(float)));
     CK(cudaMalloc(&ptrs, 3 * nimg * sizeof(float*)));
-    ws.partial_floats = conv_workspace_floats();
-    ws.n_counters = conv_workspace_counters();
-    CK(cudaMalloc(&ws.partials, ws.partial_floats * sizeof(float)));
-    CK(cudaMalloc(&ws.counters, ws.n_counters * sizeof(int)));
-    CK(cudaMemset(ws.counters, 0, ws.n_counters * sizeof(int)));
     CK(cudaMemcpy(din, in_host, in_img * nimg * sizeof(float), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dw, w_host, static_cast<size_t>(d->N) * Kpad * sizeof(float), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dout, out_host, out_img * nimg * sizeof(float), cudaMemcpyHostToDevice));
@@ -133,11 +127,11 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
       CK(cudaMalloc(&trace, 8 * 3600));
       CK(cudaMemset(trace, 0, 8 * 3600));
       p.trace = trace;
-      CK(launch_conv_tc(p, ws, 0));  // warm-up (TMEM/TMA descriptors, L2)
+      CK(launch_conv_tc(p, 0));  // warm-up (TMEM/TMA descriptors, L2)
       CK(cudaDeviceSynchronize());
       CK(cudaMemset(trace, 0, 8 * 3600));
     }
-    CK(launch_conv_tc(p, ws, 0));
+    CK(launch_conv_tc(p, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));
     if (trace) {
@@ -179,7 +173,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
       CK(cudaEventCreate(&e0));
       CK(cudaEventCreate(&e1));
       CK(cudaEventRecord(e0));
-      for (int r = 0; r < reps; ++r) CK(launch_conv_tc(p, ws, 0));
+      for (int r = 0; r < reps; ++r) CK(launch_conv_tc(p, 0));
       CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1));
       float ms = 0;
@@ -191,7 +185,6 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
 done:
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
-  cudaFree(ws.partials); cudaFree(ws.counters);
   cudaFree(din); cudaFree(dw); cudaFree(dwin); cudaFree(db); cudaFree(dout); cudaFree(dres); cudaFree(ptrs);
   return rc;
 }

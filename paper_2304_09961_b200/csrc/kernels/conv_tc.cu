@@ -8,28 +8,41 @@ namespace bs200 {
 
 namespace {
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
+
+// Per-device caches (a process may drive several GPUs).
 int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
+  static int n[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!n[dev]) {
+    int v = 148;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
-    return v;
-  }();
-  return n;
+    n[dev] = v;
+  }
+  return n[dev];
 }
 
 template <int BN, bool SPLIT, bool GROUP>
 cudaError_t launch_bn(const ConvParams& p, const ConvParams& p2, int grid, cudaStream_t stream) {
   using S = conv_tc::Cfg<BN, SPLIT>;
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(conv_tc::conv_tc_kernel<BN, SPLIT, GROUP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured[dev] = true;
   }
-  return pdl::launch(conv_tc::conv_tc_kernel<BN, SPLIT, GROUP>, dim3(grid), dim3(S::kThreads), S::kTotal, stream, p,
-                     p2);
+  // Split-K launches are clusters of ksplits CTAs (one per split of a tile).
+  const int cluster = p.ksplits > 1 ? p.ksplits : 1;
+  return pdl::launch_ex(conv_tc::conv_tc_kernel<BN, SPLIT, GROUP>, dim3(grid), dim3(S::kThreads), S::kTotal, stream,
+                        cluster, p, p2);
 }
 
 }  // namespace
@@ -60,8 +73,6 @@ void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide) {
   p.has_wide = 1;
 }
 
-std::size_t conv_workspace_floats() { return static_cast<std::size_t>(2 * 160) * conv_tc::kBM * 128; }
-int conv_workspace_counters() { return 2 * 2 * 160; }
 
 namespace {
 // The driver entry point is resolved through the runtime, so the library has
@@ -226,34 +237,33 @@ void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& g, c
 }
 
 namespace {
-// Split-K cost model: a split unit pays the partial-tile round trip and the
-// cross-CTA wait, worth ~60 K tiles of work (refit on the GoogLeNet and
-// ResNet-50 layer sums at b = 1 / 4 / 16 after the epilogue and grouping
-// changes: 24 -> 60 is -13% / -17% / -12% on GoogLeNet, +3% / -1% / -2% on
-// ResNet-50; knobs BS_CONV_KS_MAX / BS_CONV_KS_OVH). Splits only when the
-// tiles cannot cover the SMs, and keeps every split unit co-resident.
-int choose_ksplits(int tiles, int KT, int bn, int sms, const ConvWorkspace& ws) {
+// Split-K cost model. The splits of a tile are one thread-block cluster
+// (<= 8 CTAs, the portable cluster size) whose partial tiles are reduced over
+// DSMEM at the end of the kernel; a split unit costs its K tiles plus a fixed
+// overhead (partial tile into shared memory, two cluster barriers, the
+// reduction of 128 / ks rows from ks peers), in K-tile units (BS_CONV_KS_OVH,
+// default fitted on the GoogLeNet / ResNet-50 layer sums at small batches;
+// BS_CONV_KS_MAX caps the split). Splits only when the tiles cannot cover the
+// SMs, one unit per CTA.
+int choose_ksplits(int tiles, int KT, int sms) {
   int ks = 1;
-  static const int ks_max = std::getenv("BS_CONV_KS_MAX") ? std::atoi(std::getenv("BS_CONV_KS_MAX")) : 16;
-  static const int ks_ovh = std::getenv("BS_CONV_KS_OVH") ? std::atoi(std::getenv("BS_CONV_KS_OVH")) : 60;
-  if (tiles < sms && ws.partials && ws.counters && 2 * tiles <= ws.n_counters) {
+  static const int ks_max = std::min(8, std::getenv("BS_CONV_KS_MAX") ? std::atoi(std::getenv("BS_CONV_KS_MAX")) : 8);
+  static const int ks_ovh = std::getenv("BS_CONV_KS_OVH") ? std::atoi(std::getenv("BS_CONV_KS_OVH")) : 16;
+  if (tiles < sms) {
     auto cost = [&](int k) {
       const int per = (KT + k - 1) / k;
       const int units = tiles * k;
       const int waves = (units + sms - 1) / sms;
-      return waves * (per + (k > 1 ? ks_ovh : 3));
+      return waves * (per + (k > 1 ? ks_ovh : 0));
     };
     int best = cost(1);
     for (int k = 2; k <= ks_max && tiles * k <= sms && k <= KT; ++k) {
-      if (static_cast<std::size_t>(tiles) * k * conv_tc::kBM * bn > ws.partial_floats) break;
       const int c = cost(k);
       if (c < best) {
         best = c;
         ks = k;
       }
     }
-    const int per = (KT + ks - 1) / ks;
-    ks = (KT + per - 1) / per;
   }
   return ks;
 }
@@ -282,7 +292,7 @@ cudaError_t launch_dispatch(const ConvParams& p, const ConvParams& p2, int bn, i
 }
 }  // namespace
 
-cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t stream) {
+cudaError_t launch_conv_tc(ConvParams p, cudaStream_t stream) {
   if (p.Cin % 4 != 0 || p.Kpad % conv_tc::kBK != 0 || p.Kpad < p.K || p.nimg <= 0)
     return cudaErrorInvalidValue;
   int bn = conv_tile_n(p.N);
@@ -303,12 +313,11 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   }
   p.n_tiles = (p.N + bn - 1) / bn;
   const int tiles = p.m_tiles * p.n_tiles;
-  // Split K when the tiles cannot cover the SMs (small merged batches).
-  // Pick the split count minimising the estimated makespan
-  //   waves(units) * (k tiles per unit + per-unit overhead),
-  // with every unit of a split-K launch co-resident (units <= SMs) so the
-  // cooperative reduction can wait on its tile's splits.
-  const int ks = choose_ksplits(tiles, KT, bn, sms, ws);
+  // Split K when the tiles cannot cover the SMs (small merged batches):
+  // minimise the estimated makespan waves(units) * (K tiles per unit +
+  // overhead); a split launch has one CTA per unit (cluster = the splits).
+  int ks = choose_ksplits(tiles, KT, sms);
+  if (p.ks_force > 0) ks = std::min({p.ks_force, 8, KT});  // measured choice (executor autotune)
   static const int dbg = std::getenv("BS_CONV_DEBUG") ? std::atoi(std::getenv("BS_CONV_DEBUG")) : 0;
   p.debug = dbg;
   // n-minor unit order (opt-in BS_CONV_NMINOR=1): an M tile's activations
@@ -319,11 +328,8 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   const char* nm = std::getenv("BS_CONV_NMINOR");  // per launch (A/B)
   p.n_minor = nm ? (nm[0] == '1') : 0;
   p.ksplits = std::max(1, ks);
-  p.kt_per_split = (KT + p.ksplits - 1) / p.ksplits;
-  p.partials = ws.partials;
-  p.counters = ws.counters;
   const int units = tiles * p.ksplits;
-  const int grid = std::min(units, sms);
+  const int grid = p.ksplits > 1 ? units : std::min(units, sms);
   static const bool log = std::getenv("BS_CONV_LOG") != nullptr;
   if (log)
     std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d tma=%d win=%d box=%dx%dx%d g=%d\n",
@@ -332,44 +338,43 @@ cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t s
   return launch_dispatch(p, p, bn, grid, stream);
 }
 
-cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, const ConvWorkspace& ws, cudaStream_t stream) {
+cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream, bool force, int ks) {
   for (const ConvParams* q : {&a, &b})
     if (q->Cin % 4 != 0 || q->Kpad % conv_tc::kBK != 0 || q->Kpad < q->K || q->nimg <= 0 || q->a_tma ||
         q->a_win || q->tap_rows || q->split != a.split)
       return cudaErrorInvalidValue;
   const int bn = std::max(conv_tile_n(a.N), conv_tile_n(b.N));
-  // Grouping gives up split-K: decline (the caller launches the two convs
+  // Unforced, a group is unsplit: decline (the caller launches the two convs
   // separately) when either conv would be split on its own.
   for (const ConvParams* q : {&a, &b}) {
+    if (force) break;
     const int qbn = conv_tile_n(q->N);
     const int tiles = ((q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM) * ((q->N + qbn - 1) / qbn);
-    if (choose_ksplits(tiles, q->Kpad / conv_tc::kBK, qbn, sm_count(), ws) > 1) return cudaErrorNotSupported;
+    if (choose_ksplits(tiles, q->Kpad / conv_tc::kBK, sm_count()) > 1) return cudaErrorNotSupported;
     ConvParams t = *q;
     t.m_tiles = (q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM;
     if (use_wide(t, sm_count())) return cudaErrorNotSupported;  // 128 x 256 tiles beat the group
   }
   static const int dbg = std::getenv("BS_CONV_DEBUG") ? std::atoi(std::getenv("BS_CONV_DEBUG")) : 0;
+  ks = force ? std::max(1, std::min({ks, 8, a.Kpad / conv_tc::kBK, b.Kpad / conv_tc::kBK})) : 1;
   for (ConvParams* q : {&a, &b}) {
     q->m_tiles = (q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM;
     q->n_tiles = (q->N + bn - 1) / bn;
-    q->ksplits = 1;
-    q->kt_per_split = q->Kpad / conv_tc::kBK;
-    q->partials = ws.partials;
-    q->counters = ws.counters;
+    q->ksplits = ks;
     q->debug = dbg;
     q->group_units = 0;
     const char* nm = std::getenv("BS_CONV_NMINOR");
     q->n_minor = nm ? (nm[0] == '1') : 0;
   }
   b.trace = a.trace;
-  a.group_units = b.m_tiles * b.n_tiles;
-  const int units = a.m_tiles * a.n_tiles + a.group_units;
-  const int grid = std::min(units, sm_count());
+  a.group_units = b.m_tiles * b.n_tiles * ks;
+  const int units = a.m_tiles * a.n_tiles * ks + a.group_units;
+  const int grid = ks > 1 ? units : std::min(units, sm_count());
   static const bool log = std::getenv("BS_CONV_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=1 grid=%d tma=0 win=0 group=M%dN%dK%d\n",
-                 a.nimg * a.Ho * a.Wo, a.N, a.K, a.Kpad / conv_tc::kBK, bn, units, grid, b.nimg * b.Ho * b.Wo, b.N,
-                 b.K);
+    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d units=%d ks=%d grid=%d tma=0 win=0 group=M%dN%dK%d\n",
+                 a.nimg * a.Ho * a.Wo, a.N, a.K, a.Kpad / conv_tc::kBK, bn, units, ks, grid, b.nimg * b.Ho * b.Wo,
+                 b.N, b.K);
   return launch_dispatch(a, b, bn, grid, stream);
 }
 

@@ -10,9 +10,10 @@
 // unit overlap the MMAs and epilogue of the current one. The accumulator is
 // double-buffered in TMEM (2 x BN columns): the epilogue of unit i drains one
 // buffer while the MMAs of unit i+1 fill the other. Small-M layers (batches
-// of a few requests) are split along K so the grid still covers all SMs;
-// partial tiles go to a workspace and the CTA that finishes a tile last
-// reduces them in fixed split order (deterministic results).
+// of a few requests) are split along K so the grid still covers all SMs:
+// the splits of a tile form one thread-block cluster, park their partial
+// tiles in their own shared memory and reduce them over DSMEM in fixed split
+// order (deterministic results, no global workspace, no cross-CTA spin).
 //
 // Loads and operands:
 //   * B (weights, dense [N][Kpad]) by TMA, one 128B-swizzled 2D box per stage,
@@ -71,9 +72,7 @@ struct ConvParams {
   int round_out;                // round outputs to TF32 (they feed another GEMM)
   int split;                    // 1: 2xTF32 (A = A_hi + A_lo, near-fp32 accuracy)
   // work decomposition (filled by launch_conv_tc)
-  int m_tiles, n_tiles, ksplits, kt_per_split;
-  float* partials;              // [units][128][BN] split-K workspace
-  int* counters;                // [tiles] zero between launches (reset by the reducer)
+  int m_tiles, n_tiles, ksplits;  // K tiles of split s: [s KT / ksplits, (s + 1) KT / ksplits)
   unsigned long long* trace;    // debug timeline of CTA 0 (nullptr in production)
   // TMA activation path (a_tma = 1): A tiles are (Hb x Wb) output-pixel boxes
   // of one image each, loaded per filter tap by a 4D tensor map over the whole
@@ -108,19 +107,15 @@ struct ConvParams {
   // Tile-width preference from the executor's profile-time autotune:
   // 0 = launcher rule, 1 = 128 x 256 tiles (needs has_wide), 2 = 128-wide.
   int wide_pref;
+  // K-split override from the same autotune: 0 = launcher cost model, else
+  // the split count (clamped to the K tiles and the cluster limit of 8).
+  int ks_force;
   int n_minor;                  // unit order (see unit_of)
   int debug;                    // experiment switches (0 in production; BS_CONV_DEBUG)
   CUtensorMap wmap_wide;        // weights with a 256-row box (N > 128), used for 128 x 256 tiles
   int has_wide;
 };
 
-// Device workspace for split-K (owned by the caller; counters zeroed once).
-struct ConvWorkspace {
-  float* partials = nullptr;
-  std::size_t partial_floats = 0;
-  int* counters = nullptr;
-  int n_counters = 0;
-};
 
 namespace conv_tc {
 
@@ -195,8 +190,9 @@ __device__ __forceinline__ Unit unit_of(const ConvParams& p, int u, int BN, int 
   w.mt = mt;
   w.m_base = mt * kBM;
   w.n_base = nt * BN;
-  w.kt0 = w.split * p.kt_per_split;
-  w.kt1 = min(KT, w.kt0 + p.kt_per_split);
+  // balanced: every split has >= 1 K tile when ksplits <= KT
+  w.kt0 = (w.split * KT) / p.ksplits;
+  w.kt1 = ((w.split + 1) * KT) / p.ksplits;
   return w;
 }
 
@@ -326,7 +322,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   // Everything above overlapped the previous kernel's tail (PDL). The weight
   // TMA warp reads only immutable weights and starts at once; every other
-  // role touches activations / blob tables / the split-K workspace and waits
+  // role touches activations / blob tables and waits
   // for the previous kernel to complete.
   if (warp != 9) pdl::wait();
   if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x + 1] = gtime();
@@ -1008,11 +1004,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           }
         }
       } else {
-        // Split-K: park the raw partial tile; once all splits of the tile
-        // have landed (every unit of a split-K launch is co-resident: the
-        // launcher keeps units <= SMs), each split CTA reduces a slice of the
-        // tile rows in fixed split order (deterministic) and writes them.
-        float* part = p.partials + (static_cast<std::size_t>(u) * kBM + row) * BN;
+        // Split-K (cluster launch, CTA rank = split, one unit per CTA): park
+        // this split's raw partial tile in OWN shared memory -- the A ring,
+        // idle once the unit's MMAs are done -- as [row][BN] fp32 with the
+        // 16-byte chunks XOR-swizzled by row (conflict-free stores). The
+        // cluster reduces the tile over DSMEM after the role loops (below).
+        const uint32_t prow = smem_base + static_cast<uint32_t>(row * BN * 4);
 #pragma unroll 1
         for (int jj = 0; jj < BN / 32; ++jj) {
           uint32_t v[32];
@@ -1023,55 +1020,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
             ptx::mbar_arrive(&acc_empty[acc]);
           }
 #pragma unroll
-          for (int q = 0; q < 32; q += 4)
-            __stcg(reinterpret_cast<float4*>(part + jj * 32 + q),
-                   make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]), __uint_as_float(v[q + 2]),
-                               __uint_as_float(v[q + 3])));
-        }
-        __threadfence();
-        named_bar(1, 128);
-        int* arrive = p.counters + 2 * w.tile;
-        if (et == 0) {
-          atomicAdd(arrive, 1);
-          while (atomicAdd(arrive, 0) < p.ksplits) __nanosleep(64);
-        }
-        named_bar(1, 128);
-        __threadfence();
-        // Rows [r_lo, r_hi) of this tile are reduced by this split.
-        const int rows_per = (kBM + p.ksplits - 1) / p.ksplits;
-        const int r_lo = w.split * rows_per, r_hi = min(kBM, r_lo + rows_per);
-        constexpr int kVec = BN / 4;  // float4 per row
-        const std::size_t first = static_cast<std::size_t>(w.tile) * p.ksplits;
-        for (int idx = et; idx < (r_hi - r_lo) * kVec; idx += 128) {
-          const int rr = r_lo + idx / kVec;
-          const int c4 = idx - (idx / kVec) * kVec;
-          const int n0 = w.n_base + c4 * 4;
-          int img, px;
-          if (!row_pixel(p, w.mt, rr, img, px) || n0 >= p.N) continue;
-          float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int sp = 0; sp < p.ksplits; ++sp) {
-            const float4 x = __ldcg(reinterpret_cast<const float4*>(
-                p.partials + ((first + sp) * kBM + rr) * BN + c4 * 4));
-            acc4.x += x.x;
-            acc4.y += x.y;
-            acc4.z += x.z;
-            acc4.w += x.w;
-          }
-          float* orow = p.out_ptrs[img] + p.out_off + static_cast<long>(px) * p.out_ldc;
-          const float* rrow = p.res_ptrs ? p.res_ptrs[img] + p.res_off + static_cast<long>(px) * p.res_ldc : nullptr;
-          const float vals[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (n0 + q < p.N) orow[n0 + q] = epilogue_op(p, vals[q], n0 + q, rrow);
-        }
-        // Last split out resets the tile's counters for the next launch.
-        named_bar(1, 128);
-        if (et == 0) {
-          __threadfence();
-          if (atomicAdd(p.counters + 2 * w.tile + 1, 1) == p.ksplits - 1) {
-            p.counters[2 * w.tile] = 0;
-            p.counters[2 * w.tile + 1] = 0;
-          }
+          for (int q = 0; q < 8; ++q)
+            ptx::sts128(prow + static_cast<uint32_t>(((jj * 8 + q) ^ (row & 7)) << 4),
+                        make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                    __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
         }
       }
     }
@@ -1140,6 +1092,47 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem_base);
   }
+  if (p.ksplits > 1) {
+    // ------------------------------------------ split-K reduction over DSMEM
+    // The ks CTAs of a cluster hold the ks K-splits of one tile (the
+    // hardware co-schedules a cluster, so no CTA ever waits for one that is
+    // not resident -- unlike a grid-wide spin, this cannot deadlock against
+    // other work on the GPU). After the barrier every partial is visible;
+    // CTA `rank` reduces rows [rank * 128 / ks, ...) in fixed split order
+    // (deterministic), applies bias / residual / activation and writes them.
+    // The second barrier keeps every CTA's shared memory alive until all
+    // peers have read it.
+    ptx::cluster_sync_all();
+    const int rank = static_cast<int>(ptx::cluster_ctarank());
+    BS_UNIT_PROBLEM(static_cast<int>(blockIdx.x))
+    const Unit w = unit_of(p, lu, BN, KT);
+    const int rows_per = (kBM + p.ksplits - 1) / p.ksplits;
+    const int r_lo = rank * rows_per, r_hi = min(kBM, r_lo + rows_per);
+    constexpr int kVec = BN / 4;  // 16-byte chunks per row
+    for (int idx = threadIdx.x; idx < (r_hi - r_lo) * kVec; idx += blockDim.x) {
+      const int rr = r_lo + idx / kVec;
+      const int c4 = idx - (idx / kVec) * kVec;
+      const int n0 = w.n_base + c4 * 4;
+      int img, px;
+      if (!row_pixel(p, w.mt, rr, img, px) || n0 >= p.N) continue;
+      const uint32_t off = smem_base + static_cast<uint32_t>(rr * BN * 4 + ((c4 ^ (rr & 7)) << 4));
+      float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int sp = 0; sp < p.ksplits; ++sp) {
+        const float4 x = ptx::ld_dsmem128(ptx::mapa_shared(off, static_cast<uint32_t>(sp)));
+        acc4.x += x.x;
+        acc4.y += x.y;
+        acc4.z += x.z;
+        acc4.w += x.w;
+      }
+      float* orow = p.out_ptrs[img] + p.out_off + static_cast<long>(px) * p.out_ldc;
+      const float* rrow = p.res_ptrs ? p.res_ptrs[img] + p.res_off + static_cast<long>(px) * p.res_ldc : nullptr;
+      const float vals[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (n0 + q < p.N) orow[n0 + q] = epilogue_op(p, vals[q], n0 + q, rrow);
+    }
+    ptx::cluster_sync_all();
+  }
 }
 
 }  // namespace conv_tc
@@ -1195,12 +1188,14 @@ void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide);
 // Grouped launch of two independent convs (no data flow between them; same
 // precision; cp.async gather path, no split-K): one persistent grid walks the
 // units of a, then of b, with a common tile width.
-cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, const ConvWorkspace& ws, cudaStream_t stream);
-// Host-side launcher: chooses the K split, grid and workspace use
+// force: launch grouped even where the launcher's rules would decline (the
+// executor's autotune measured the group faster at this batch).
+// ks > 0 (with force): split both convs ks ways (cluster of ks CTAs per tile;
+// clamped to the shorter K loop).
+cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream, bool force = false, int ks = 1);
+// Host-side launcher: chooses the K split (a split-K launch is a cluster
+// launch, one CTA per split, reduced over DSMEM) and the grid
 // (p.wmap must be encoded for conv_tile_n(p.N)).
-cudaError_t launch_conv_tc(ConvParams p, const ConvWorkspace& ws, cudaStream_t stream);
-// Workspace sizing for the largest split-K decomposition the launcher uses.
-std::size_t conv_workspace_floats();
-int conv_workspace_counters();
+cudaError_t launch_conv_tc(ConvParams p, cudaStream_t stream);
 
 }  // namespace bs200

@@ -245,26 +245,46 @@ __global__ void maxpool_rows_kernel(const PoolParams p) {
 }
 
 // One thread per (image, 4 channels); sums the H*W pixels in fp32.
+// Global average pool. One CTA per (image, 32 channel quads): the 8 warps
+// split the pixels (lane = channel quad, so each pixel row read is 512
+// contiguous bytes), then the 8 partial sums are folded in shared memory in
+// a fixed order. At small batches this keeps ~8 CTAs per image in flight
+// instead of one thread per channel quad walking all pixels serially.
 __global__ void avgpool_kernel(const AvgPoolParams p) {
   pdl::launch_dependents();
   pdl::wait();
+  __shared__ float4 part[8][32];
   const int C4 = p.C >> 2;
-  const long total = static_cast<long>(p.nimg) * C4;
-  const float inv = 1.0f / static_cast<float>(p.HW);
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int c4 = static_cast<int>(i % C4);
-    const int n = static_cast<int>(i / C4);
+  const int chunks = (C4 + 31) / 32;
+  const int n = blockIdx.x / chunks;
+  const int c4 = (blockIdx.x - n * chunks) * 32 + (threadIdx.x & 31);
+  const int wg = threadIdx.x >> 5;  // pixel group 0..7
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c4 < C4) {
     const float* in = p.in_ptrs[n] + p.in_off + c4 * 4;
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int q = 0; q < p.HW; ++q) {
+#pragma unroll 4
+    for (int q = wg; q < p.HW; q += 8) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(in + static_cast<long>(q) * p.in_ldc));
       s.x += v.x;
       s.y += v.y;
       s.z += v.z;
       s.w += v.w;
     }
-    float4 o = make_float4(s.x * inv, s.y * inv, s.z * inv, s.w * inv);
+  }
+  part[wg][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (wg == 0 && c4 < C4) {
+    float4 t = part[0][threadIdx.x];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) {
+      const float4 v = part[g][threadIdx.x];
+      t.x += v.x;
+      t.y += v.y;
+      t.z += v.z;
+      t.w += v.w;
+    }
+    const float inv = 1.0f / static_cast<float>(p.HW);
+    float4 o = make_float4(t.x * inv, t.y * inv, t.z * inv, t.w * inv);
     if (p.round_out) {
       o.x = ptx::round_tf32(o.x);
       o.y = ptx::round_tf32(o.y);
@@ -401,22 +421,35 @@ __global__ void __launch_bounds__(256) dwconv3_block_kernel(const DwParams p) {
 }
 
 // One warp per image: max, sum of exp, normalise.
+// Softmax over N classes, one CTA (256 threads) per image: block max and
+// block sum through shared memory (fixed reduction order).
 __global__ void softmax_kernel(const SoftmaxParams p) {
   pdl::launch_dependents();
   pdl::wait();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= p.nimg) return;
-  const float* x = p.ptrs[warp] + p.in_off;
-  float* y = const_cast<float*>(p.ptrs[warp]) + p.out_off;
+  __shared__ float red[8];
+  const int n = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* x = p.ptrs[n] + p.in_off;
+  float* y = const_cast<float*>(p.ptrs[n]) + p.out_off;
   float m = -FLT_MAX;
-  for (int j = lane; j < p.N; j += 32) m = fmaxf(m, x[j]);
+  for (int j = threadIdx.x; j < p.N; j += blockDim.x) m = fmaxf(m, x[j]);
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+  __syncthreads();
   float s = 0.f;
-  for (int j = lane; j < p.N; j += 32) s += __expf(x[j] - m);
+  for (int j = threadIdx.x; j < p.N; j += blockDim.x) s += __expf(x[j] - m);
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  s = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) s += red[w];
   const float inv = 1.f / s;
-  for (int j = lane; j < p.N; j += 32) y[j] = __expf(x[j] - m) * inv;
+  for (int j = threadIdx.x; j < p.N; j += blockDim.x) y[j] = __expf(x[j] - m) * inv;
 }
 
 __global__ void gather_out_kernel(const GatherParams p) {
@@ -481,7 +514,7 @@ cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {
 cudaError_t launch_avgpool(const AvgPoolParams& p, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   if (p.C % 4) return cudaErrorInvalidValue;
-  e = pdl::launch(avgpool_kernel, dim3(grid_for(static_cast<long>(p.nimg) * (p.C / 4))), dim3(kThreads), 0, s, p);
+  e = pdl::launch(avgpool_kernel, dim3(p.nimg * ((p.C / 4 + 31) / 32)), dim3(256), 0, s, p);
   return e;
 }
 
@@ -506,8 +539,7 @@ cudaError_t launch_gather_out(const GatherParams& p, cudaStream_t s) {
 
 cudaError_t launch_softmax(const SoftmaxParams& p, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
-  const int blocks = (p.nimg * 32 + kThreads - 1) / kThreads;
-  e = pdl::launch(softmax_kernel, dim3(blocks), dim3(kThreads), 0, s, p);
+  e = pdl::launch(softmax_kernel, dim3(p.nimg), dim3(256), 0, s, p);
   return e;
 }
 

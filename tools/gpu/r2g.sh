@@ -1,0 +1,5 @@
+mkdir -p gpurun_out/r2
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2/pytest_g.txt 2>&1; tail -n 5 gpurun_out/r2/pytest_g.txt
+TUNE_LOG=gpurun_out/r2/tunelog2 timeout 900 python tools/tuned_span.py small_cnn:1,10 googlenet:1,4,8,16,32,90 resnet50:1,8,32,90 mobilenet_v2:1,8,32 > gpurun_out/r2/tuned_span2.txt 2>&1
+cat gpurun_out/r2/tuned_span2.txt
+timeout 600 ncu --nvtx --nvtx-include "pass/" --cache-control none --clock-control none --metrics gpu__time_duration.sum --csv --log-file gpurun_out/r2/pass2_goog_b1.csv python tools/pass_launches.py googlenet 1 > /dev/null 2>&1
