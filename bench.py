@@ -166,7 +166,8 @@ def run_ours(a, ws, rank, local) -> dict | None:
     ex.set_precision(a.precision)
     # The executor first autotunes each N > 128 conv's tile width per batch
     # (kept for the run), then measures the latency table the scheduler uses.
-    prof = ex.profile_table(batches=[b for b in BATCHES if b < mb] + [mb], reps=10, tune_tiles=True)
+    prof = ex.profile_table(batches=[b for b in BATCHES if b < mb] + [mb], reps=10, tune_tiles=True,
+                            flush_l2=a.table_flush_l2)
     prof.pop("tile_tune", None)
     names = [n["name"] for n in ex.desc["nets"]]
     comp = {c["id"]: c for c in prof["components"]}
@@ -177,9 +178,13 @@ def run_ours(a, ws, rank, local) -> dict | None:
     t1 = max(dnn_ms(d, 1) for d in prof["dnns"])
     tmax = max(dnn_ms(d, mb) for d in prof["dnns"])
     # D = 6.25 x T1 (the paper's 150 ms / 24 ms ratio), T1 =
-    # the single-request latency of the slowest DNN in the table measured at
-    # startup; --deadline-ms overrides it (reported).
-    deadline = a.deadline_ms if a.deadline_ms else round(6.25 * t1, 3)
+    # the single-request latency of the slowest DNN in the committed B200
+    # table of this config (profiles/r02, measured by this executor; the
+    # reference arm simulates on the same table, so both arms serve the same
+    # deadline); the fresh startup table's T1 is reported beside it and used
+    # when no table is committed. --deadline-ms overrides (reported).
+    t1_table = committed_t1(a.config)
+    deadline = a.deadline_ms if a.deadline_ms else round(6.25 * (t1_table or t1), 3)
     sim = {"scheduler": cfg["scheduler"], "granularity": cfg["granularity"], "max_batch": mb}
     if "shared_batching" in cfg:
         sim["shared_batching"] = cfg["shared_batching"]
@@ -242,7 +247,9 @@ def run_ours(a, ws, rank, local) -> dict | None:
         ex.stats(False)
         cap *= 0.96
     clocks = clk.summary()
-    stats = ex.stats_summary(pk["hbm_gbs"], pk["tf32_tflops"])
+    # tensor peak of the arithmetic this run uses (BF16: the measured bf16 rate)
+    tc_peak = pk["bf16_tflops_sustained"] if a.precision == "bf16" else pk["tf32_tflops"]
+    stats = ex.stats_summary(pk["hbm_gbs"], tc_peak)
     ex.stats(False)
 
     # ---- e2e: same runs through the C-ABI with H2D inputs / D2H results.
@@ -284,27 +291,32 @@ def run_ours(a, ws, rank, local) -> dict | None:
         tensor_bound = conv["ideal_tensor_ms"] >= conv["ideal_hbm_ms"]
         if tensor_bound:
             ach = conv["flops"] / (conv["ms"] * 1e-3) / 1e12
-            roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk["tf32_tflops"], "unit": "TFLOP/s"}
+            roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": tc_peak, "unit": "TFLOP/s"}
         else:
             ach = conv["bytes"] / (conv["ms"] * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s"}
         roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
         roof["frac_of_roofline_mixed"] = round(conv["ideal_ms"] / conv["ms"], 4)
-        roof["kernel"] = "conv_tc_kernel (tcgen05 TF32 implicit GEMM, 2xTF32 split-A)"
+        roof["kernel"] = {"tf32x2": "conv_tc_kernel (tcgen05 TF32 implicit GEMM, 2xTF32 split-A)",
+                          "tf32": "conv_tc_kernel (tcgen05 TF32 implicit GEMM)",
+                          "bf16": "conv_tc_kernel (tcgen05 kind::f16 BF16 implicit GEMM)"}[a.precision]
         roof["sampled_launches"] = conv["launches"]
         roof["avg_launch_us"] = round(conv["ms"] / conv["launches"] * 1000, 2)
-        roof["peak_source"] = f"{pk['source']}: tf32 = bf16_tflops_sustained / 2; hbm_gbs measured copy"
+        roof["peak_source"] = (f"{pk['source']}: " + ("bf16_tflops_sustained" if a.precision == "bf16" else
+                               "tf32 = bf16_tflops_sustained / 2") + "; hbm_gbs measured copy")
         roof["traffic"] = ncu_traffic()
         # The TF32 MMA rate measured on this part (profiles/r01/micro_b200.txt,
         # tools/micro/mma_micro.cu: one 128x128x8 MMA per 64 cycles per SM) at
         # the SM clock sampled during the run. 2xTF32 issues two MMAs per
-        # algorithmic MAC, so tensor_pipe_frac = 2 * achieved / this rate.
+        # algorithmic MAC, so tensor_pipe_frac = 2 * achieved / this rate;
+        # BF16 MMAs run at twice the TF32 rate, one per MAC.
         import torch
         sms = torch.cuda.get_device_properties(0).multi_processor_count
         mhz = (clocks or {}).get("sm_mhz") or 1965.0
         mma_rate = 2 * 128 * 128 * 8 / 64 * sms * mhz * 1e6 / 1e12
         roof["tf32_mma_rate_measured"] = round(mma_rate, 1)
-        roof["tensor_pipe_frac"] = round(2 * ach / mma_rate, 4) if tensor_bound else None
+        passes_per_rate = {"tf32x2": 2.0, "tf32": 1.0, "bf16": 0.5}[a.precision]
+        roof["tensor_pipe_frac"] = round(passes_per_rate * ach / mma_rate, 4) if tensor_bound else None
         total_ms = sum(v["ms"] for v in stats.values())
         roof["share_of_device_time"] = round(conv["ms"] / total_ms, 4) if total_ms else None
 
@@ -322,7 +334,8 @@ def run_ours(a, ws, rank, local) -> dict | None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32 (tf32x2 tcgen05 MMA, fp32 accumulate)" if a.precision == "tf32x2" else "f32 (tf32 MMA)",
+        "dtype": {"tf32x2": "f32 (tf32x2 tcgen05 MMA, fp32 accumulate)", "tf32": "f32 (tf32 MMA)",
+                  "bf16": "bf16 (bf16 tcgen05 MMA operands, fp32 accumulate, fp32 activations)"}[a.precision],
         "data": "synthetic images (SplitMix64 N(0,1)), deterministic random-init weights",
         "on_time_ratio": round(tot_on / tot_gen, 4) if tot_gen else None,
         "config": {
@@ -333,9 +346,14 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "requests_per_step": a.requests,
             "deadline_ms": round(deadline, 4),
             "t1_ms": round(t1, 4),
+            "t1_ms_committed_table": round(t1_table, 4) if t1_table else None,
+            "deadline_rule": "6.25 x T1 of the committed table" if (t1_table and not a.deadline_ms) else
+                             ("override" if a.deadline_ms else "6.25 x T1 of the startup table"),
             "t_max_batch_ms": round(t90, 4),
             "max_batch": mb,
             "precision": a.precision,
+            "latency_table": "cold L2 (flushed before every timed layer)" if a.table_flush_l2 else
+                             "warm L2 (median of back-to-back repetitions)",
             "l2": "no flush: each step touches R x 4.6 MB request blobs (>> 126 MB L2) plus 26 MB of weights",
             "parallelism": f"{ws} independent servers (request streams sharded, no collectives)",
         },
@@ -356,7 +374,8 @@ def run_ours(a, ws, rank, local) -> dict | None:
         "kernel_stats": stats,
         "wall_ms_timed": round(wall_ms, 1),
     }
-    out["layer_rooflines"] = layer_rooflines(ex.desc, prof, pk) if len(names) == 1 else None
+    out["layer_rooflines"] = layer_rooflines(ex.desc, prof, pk, tc_peak=tc_peak,
+                                             w_bytes=2.0 if a.precision == "bf16" else 4.0) if len(names) == 1 else None
     if a.dump_table:
         Path(a.dump_table).parent.mkdir(parents=True, exist_ok=True)
         Path(a.dump_table).write_text(json.dumps(dict(prof, _meta={
@@ -386,6 +405,17 @@ TABLES = {1: ROOT / "profiles" / "r02" / "small_cnn_table_b200.json",
           2: ROOT / "profiles" / "r02" / "googlenet_table_b200.json",
           3: ROOT / "profiles" / "r02" / "resnet50_pair_table_b200.json",
           4: ROOT / "profiles" / "r02" / "hetero3_table_b200.json"}
+
+
+def committed_t1(config: int) -> float | None:
+    """T1 (single-request latency, slowest DNN) of the committed B200 table."""
+    table = TABLES.get(config)
+    if table is None or not table.exists():
+        return None
+    prof = json.loads(table.read_text())
+    comp = {c["id"]: c for c in prof["components"]}
+    return max(sum(dict(L["runtime_ms"])[1] for cid in d["stages"] for L in comp[cid]["layers"])
+               for d in prof["dnns"])
 
 
 def cpu_model() -> str:
@@ -440,12 +470,15 @@ def capacity_search(serve, est: float, min_runs: int, max_runs: int = 14):
     return (lo if lo is not None else rate), runs
 
 
-def layer_rooflines(desc: dict, prof: dict, pk: dict, batches=(1, 8, 32, 90)) -> dict:
+def layer_rooflines(desc: dict, prof: dict, pk: dict, batches=(1, 8, 32, 90), tc_peak: float | None = None,
+                    w_bytes: float = 4.0) -> dict:
     """Per-layer achieved GB/s and roofline fraction from the measured h_k(b)
     table (CUDA events around each layer, tools: Executor.profile_table).
     Algorithmic work per layer: bytes = weights + bias once +
-    b x (in + out + residual) activations, fp32; FLOPs = 2 b MACs. Ideal time
-    = max(bytes / HBM peak, FLOPs / TF32 peak); frac = ideal / measured."""
+    b x (in + out + residual) activations, fp32 (weights w_bytes each: 2 for
+    the bf16 path); FLOPs = 2 b MACs. Ideal time = max(bytes / HBM peak,
+    FLOPs / tensor peak of the precision); frac = ideal / measured."""
+    tc_peak = tc_peak or pk["tf32_tflops"]
     net = desc["nets"][0]
     comp = {c["id"]: c for c in prof["components"]}
     times = [dict(L["runtime_ms"]) for cid in prof["dnns"][0]["stages"] for L in comp[cid]["layers"]]
@@ -472,10 +505,11 @@ def layer_rooflines(desc: dict, prof: dict, pk: dict, batches=(1, 8, 32, 90)) ->
                 act = elems(op["in"], False, op) + elems(op["res"], True, op)
                 act += op["in"][2] if op["kind"] == "avgpool" else (op["out"][2] if op["kind"] == "softmax"
                                                                     else elems(op["out"], True, op))
-                by += 4.0 * (w + b * act)
+                by += w_bytes * op["weight_floats"] + 4.0 * (w - op["weight_floats"] + b * act) \
+                    if op["kind"] == "conv" else 4.0 * (w + b * act)
                 fl += op["flops"] * b
             ms = times[k][b]
-            ideal = max(by / (pk["hbm_gbs"] * 1e9), fl / (pk["tf32_tflops"] * 1e12)) * 1e3
+            ideal = max(by / (pk["hbm_gbs"] * 1e9), fl / (tc_peak * 1e12)) * 1e3
             sum_ideal += ideal
             sum_ms += ms
             rows.append([L["name"], round(ms * 1e3, 1), round(by / (ms * 1e-3) / 1e9, 1),
@@ -616,10 +650,12 @@ def main() -> None:
     ap.add_argument("--requests", type=int, default=3000, help="requests per timed step")
     ap.add_argument("--warm-requests", type=int, default=3000, help="requests per capacity-search run")
     ap.add_argument("--slots", type=int, default=4096, help="activation-arena slots")
-    ap.add_argument("--precision", default="tf32x2", choices=["tf32x2", "tf32"])
+    ap.add_argument("--precision", default="tf32x2", choices=["tf32x2", "tf32", "bf16"])
     ap.add_argument("--stats-every", type=int, default=4)
     ap.add_argument("--cpu-forward", type=int, default=1, help="time the CPU fp32 forward at b = 1 / 10 / 90")
     ap.add_argument("--dump-table", default=None, help="write the measured latency table here")
+    ap.add_argument("--table-flush-l2", type=int, default=0,
+                    help="measure the scheduler's latency table with L2 flushed before every timed layer (cold)")
     ap.add_argument("--deadline-ms", type=float, default=None, help="override D = 6.25 x T1")
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
                     help="BASELINE.json config to serve (2 = the headline line)")

@@ -72,8 +72,9 @@ void bs_free(char* p);
  * "resnet50_pair", "hetero3", "collab". max_requests = arena slots. */
 int bs_create(int device, const char* suite, int max_batch, int max_requests, bs_handle** out);
 int bs_destroy(bs_handle* h);
-/* "tf32x2" (default; split-A 2xTF32 GEMMs, fp32 activations, fp32 parity)
- * or "tf32" (one TF32 MMA per K step, TF32-rounded activations). */
+/* "tf32x2" (default; split-A 2xTF32 GEMMs, fp32 activations, fp32 parity),
+ * "tf32" (one TF32 MMA per K step, TF32-rounded activations) or "bf16"
+ * (bf16 operands, fp32 accumulation and activations; reported separately). */
 int bs_set_precision(bs_handle* h, const char* mode);
 /* JSON: DNNs, layers, ops, tensor plan, weight offsets (for checkers). */
 int bs_suite_json(bs_handle* h, char** out_json);
@@ -135,7 +136,7 @@ typedef struct bs_conv_desc {
   int res_ldc, res_coff;
   int relu;           /* 0 none, 1 relu, 2 relu6 */
   int round_out;      /* round outputs to TF32 */
-  int split;          /* 2xTF32 split-A GEMM */
+  int split;          /* precision: 0 TF32, 1 2xTF32 split-A GEMM, 2 BF16 operands */
 } bs_conv_desc;
 
 /* Runs the conv kernel once on host buffers (weights [N][Kpad], Kpad =

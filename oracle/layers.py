@@ -15,6 +15,15 @@ from __future__ import annotations
 import numpy as np
 
 
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """Round fp32 to bf16 (8-bit mantissa), nearest-even, kept as fp32 -- the
+    rounding of PTX cvt.rn.bf16x2.f32 / __float2bfloat16_rn (finite x)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
 def round_tf32(x: np.ndarray) -> np.ndarray:
     """Round fp32 to TF32 (10-bit mantissa), nearest, ties away from zero —
     the rounding of PTX cvt.rna.tf32.f32."""

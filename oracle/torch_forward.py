@@ -20,10 +20,15 @@ import torch.nn.functional as F
 
 
 class TorchNet:
-    def __init__(self, desc: dict, net: int, weights: np.ndarray, dtype=torch.float64):
+    def __init__(self, desc: dict, net: int, weights: np.ndarray, dtype=torch.float64, bf16_convs: bool = False):
+        """bf16_convs: emulate the executor's BF16 precision -- every conv / FC
+        multiplies bf16-rounded (nearest-even) activations and weights with
+        high-precision accumulation; bias, residual, pools, depthwise convs and
+        the stored activations stay fp32."""
         self.d = desc["nets"][net]
         self.w = torch.from_numpy(np.asarray(weights, np.float32))
         self.dtype = dtype
+        self.bf16_convs = bf16_convs
 
     def _get(self, env, ref):
         t, coff, c = ref
@@ -49,6 +54,9 @@ class TorchNet:
                 w = self.w[op["w_off"]:op["w_off"] + cout * op["Kpad"]].reshape(cout, op["Kpad"])[:, :K]
                 w = w.reshape(cout, k, k, cin).permute(0, 3, 1, 2).to(self.dtype)
                 b = self.w[op["b_off"]:op["b_off"] + cout].to(self.dtype)
+                if self.bf16_convs:
+                    xin = xin.to(torch.bfloat16).to(self.dtype)
+                    w = w.to(torch.bfloat16).to(self.dtype)
                 y = F.conv2d(xin, w, b, stride=op["stride"], padding=op["pad"])
                 if op["res"][0] >= 0:
                     y = y + self._get(env, op["res"])

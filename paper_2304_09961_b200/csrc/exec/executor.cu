@@ -167,6 +167,7 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
         where.emplace_back(n, i);
       }
     }
+    tap_pool_floats_ = pool.size();
     if (!pool.empty()) {
       ck(cudaMalloc(&d_tap_weights_, pool.size() * sizeof(float)), "tap-row weights");
       ck(cudaMemcpy(d_tap_weights_, pool.data(), pool.size() * sizeof(float), cudaMemcpyHostToDevice),
@@ -300,6 +301,8 @@ Executor::~Executor() {
   cudaFree(d_weights_);
   cudaFree(d_win_weights_);
   cudaFree(d_tap_weights_);
+  cudaFree(d_weights_bf16_);
+  cudaFree(d_tap_weights_bf16_);
   cudaFree(arena_);
   cudaFree(scratch_ptrs_);
   cudaFree(flush_);
@@ -320,9 +323,56 @@ void Executor::sync() {
 }
 
 void Executor::set_precision(const std::string& mode) {
-  if (mode == "tf32x2") split_ = true;
-  else if (mode == "tf32") split_ = false;
-  else throw std::invalid_argument("unknown precision '" + mode + "' (tf32x2 | tf32)");
+  if (mode == "tf32x2") prec_ = 1;
+  else if (mode == "tf32") prec_ = 0;
+  else if (mode == "bf16") {
+    build_bf16();
+    prec_ = 2;
+  } else {
+    throw std::invalid_argument("unknown precision '" + mode + "' (tf32x2 | tf32 | bf16)");
+  }
+}
+
+void Executor::build_bf16() {
+  if (bf16_ready_) return;
+  ck(cudaMalloc(&d_weights_bf16_, suite_.weights.size() * 2), "bf16 weights");
+  ck(launch_to_bf16(d_weights_, d_weights_bf16_, suite_.weights.size(), stream_), "bf16 weights");
+  if (tap_pool_floats_) {
+    ck(cudaMalloc(&d_tap_weights_bf16_, tap_pool_floats_ * 2), "bf16 tap-row weights");
+    ck(launch_to_bf16(d_tap_weights_, d_tap_weights_bf16_, tap_pool_floats_, stream_), "bf16 tap-row weights");
+  }
+  ck(cudaStreamSynchronize(stream_), "bf16 weights");
+  wmaps_bf_.assign(suite_.nets.size(), {});
+  wmaps_wide_bf_.assign(suite_.nets.size(), {});
+  gmaps_bf_.assign(suite_.nets.size(), {});
+  for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
+    const NetDef& net = suite_.nets[n];
+    wmaps_bf_[n].resize(net.ops.size());
+    wmaps_wide_bf_[n].resize(net.ops.size());
+    gmaps_bf_[n].resize(net.ops.size());
+    for (std::size_t i = 0; i < net.ops.size(); ++i) {
+      const OpDef& op = net.ops[i];
+      if (op.kind != OpKind::conv) continue;
+      const std::uint16_t* w = d_weights_bf16_ + op.w_off;
+      bool ok = encode_weight_map_bf16(&wmaps_bf_[n][i], w, op.out.C, op.Kpad);
+      if (op.out.C > 128) ok = ok && encode_weight_map_bf16(&wmaps_wide_bf_[n][i], w, op.out.C, op.Kpad, 256);
+      if (gmap_ok_[n][i]) {
+        // the group's tile width: the wider of the pair (plan_groups)
+        int bn = conv_tile_n(op.out.C);
+        for (const auto& items : plans_[n])
+          for (const LayerItem& it : items)
+            if (it.b >= 0 && (it.a == static_cast<int>(i) || it.b == static_cast<int>(i)))
+              bn = std::max(conv_tile_n(net.ops[static_cast<std::size_t>(it.a)].out.C),
+                            conv_tile_n(net.ops[static_cast<std::size_t>(it.b)].out.C));
+        ok = ok && encode_weight_map_bf16(&gmaps_bf_[n][i], w, op.out.C, op.Kpad, bn);
+      }
+      if (n < taps_.size() && i < taps_[n].size() && taps_[n][i].ok)
+        ok = ok && encode_weight_map_bf16(&taps_[n][i].wmap_bf, d_tap_weights_bf16_ + taps_[n][i].w_off, op.out.C,
+                                          op.KH * 32);
+      if (!ok) throw std::runtime_error("bf16 weight tensor maps failed for " + op.name);
+    }
+  }
+  bf16_ready_ = true;
 }
 
 // ------------------------------------------------------------------ tables
@@ -346,10 +396,13 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
   const auto ldc = [&](const TRef& r) -> int { return r.t < 0 ? 0 : net.tensors[static_cast<std::size_t>(r.t)].C; };
   const TensorDef& ti = net.tensors[static_cast<std::size_t>(op.in.t)];
   ConvParams p{};
-  p.wmap = wmaps_[static_cast<std::size_t>(&net - suite_.nets.data())][static_cast<std::size_t>(&op - net.ops.data())];
-  if (op.out.C > 128)
-    conv_add_wide_map(p, wmaps_wide_[static_cast<std::size_t>(&net - suite_.nets.data())]
-                                    [static_cast<std::size_t>(&op - net.ops.data())]);
+  const bool bf = prec_ == 2;
+  {
+    const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
+    const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
+    p.wmap = bf ? wmaps_bf_[ni][oi] : wmaps_[ni][oi];
+    if (op.out.C > 128) conv_add_wide_map(p, bf ? wmaps_wide_bf_[ni][oi] : wmaps_wide_[ni][oi]);
+  }
   p.nimg = batch;
   p.H = ti.H;
   p.W = ti.W;
@@ -375,8 +428,8 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
   p.res_off = off(op.res);
   p.res_ldc = ldc(op.res);
   p.relu = op.relu;
-  p.round_out = split_ ? 0 : op.round_out;
-  p.split = split_ ? 1 : 0;
+  p.round_out = prec_ == 0 ? op.round_out : 0;
+  p.prec = prec_;
   {
     const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
     const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
@@ -394,16 +447,18 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
   {
     const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
     const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
-    if (ni < wins_.size() && oi < wins_[ni].size() && wins_[ni][oi].ok)
+    if (bf) {
+      // BF16: cp.async gather (+ tap rows); the opt-in TMA activation modes are fp32 only
+    } else if (ni < wins_.size() && oi < wins_[ni].size() && wins_[ni][oi].ok)
       conv_use_window(p, wins_[ni][oi].amap, wins_[ni][oi].wmap, wins_[ni][oi].geom, arena_,
                       static_cast<long>(slot_floats_), total_slots_);
     else if (ni < amaps_.size() && oi < amaps_[ni].size() && amaps_[ni][oi].ok)
       conv_use_act_map(p, amaps_[ni][oi].map, amaps_[ni][oi].geom, arena_, static_cast<long>(slot_floats_),
                        total_slots_);
-    else if (ni < taps_.size() && oi < taps_[ni].size() && taps_[ni][oi].ok) {
+    if (ni < taps_.size() && oi < taps_[ni].size() && taps_[ni][oi].ok && !p.a_tma) {
       p.tap_rows = 1;
       p.Kpad = op.KH * 32;
-      p.wmap = taps_[ni][oi].wmap;
+      p.wmap = bf ? taps_[ni][oi].wmap_bf : taps_[ni][oi].wmap;
       p.wgt = d_tap_weights_ + taps_[ni][oi].w_off;
     }
   }
@@ -432,8 +487,8 @@ void Executor::launch_group(const NetDef& net, int layer, int item, const OpDef&
   }
   ConvParams pa = conv_params(net, a, d_ptrs, batch), pb = conv_params(net, b, d_ptrs, batch);
   const std::size_t ia = static_cast<std::size_t>(&a - net.ops.data()), ib = static_cast<std::size_t>(&b - net.ops.data());
-  if (gmap_ok_[ni][ia]) pa.wmap = gmaps_[ni][ia];
-  if (gmap_ok_[ni][ib]) pb.wmap = gmaps_[ni][ib];
+  if (gmap_ok_[ni][ia]) pa.wmap = prec_ == 2 ? gmaps_bf_[ni][ia] : gmaps_[ni][ia];
+  if (gmap_ok_[ni][ib]) pb.wmap = prec_ == 2 ? gmaps_bf_[ni][ib] : gmaps_[ni][ib];
   LaunchStat st{};
   const bool sample = stats_on_ && (++stats_seen_ % stats_every_ == 0) && ev_next_ + 2 <= event_pool_.size();
   if (sample) {
@@ -493,14 +548,14 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
       break;
     }
     case OpKind::avgpool: {
-      AvgPoolParams p{batch, ti.H * ti.W, op.in.C, d_ptrs, off(op.in), ldc(op.in), d_ptrs, off(op.out), split_ ? 0 : 1};
+      AvgPoolParams p{batch, ti.H * ti.W, op.in.C, d_ptrs, off(op.in), ldc(op.in), d_ptrs, off(op.out), prec_ == 0 ? 1 : 0};
       e = launch_avgpool(p, stream_);
       break;
     }
     case OpKind::dwconv: {
       DwParams p{batch, ti.H, ti.W, op.in.C, op.Ho, op.Wo, op.stride, d_ptrs, off(op.in), ldc(op.in),
                  d_weights_ + op.w_off, d_weights_ + op.b_off, d_ptrs, off(op.out), ldc(op.out), op.relu,
-                 split_ ? 0 : op.round_out};
+                 prec_ == 0 ? op.round_out : 0};
       e = launch_dwconv(p, stream_);
       break;
     }

@@ -98,9 +98,12 @@ class Executor {
   void sync();
 
   // "tf32x2" (default): split-A 2xTF32 GEMMs, fp32 activations (fp32 parity);
-  // "tf32": one TF32 MMA per K step, activations rounded to TF32.
+  // "tf32": one TF32 MMA per K step, activations rounded to TF32;
+  // "bf16": bf16 operands (activations rounded to bf16 on their way into
+  // TMEM, bf16 copies of the weights), fp32 accumulation and fp32
+  // activations in HBM -- the separately reported bf16 path.
   void set_precision(const std::string& mode);
-  const char* precision() const { return split_ ? "tf32x2" : "tf32"; }
+  const char* precision() const { return prec_ == 1 ? "tf32x2" : prec_ == 2 ? "bf16" : "tf32"; }
 
   // Device-resident synthetic image pool (inputs resident in HBM for the
   // bench); image i of dnn d.
@@ -216,6 +219,7 @@ class Executor {
   struct TapRowMap {
     bool ok = false;
     CUtensorMap wmap{};
+    CUtensorMap wmap_bf{};  // bf16 copy (BF16 precision)
     std::size_t w_off = 0;  // into d_tap_weights_
   };
   std::vector<std::vector<TapRowMap>> taps_;      // [net][op] tap-row mode (stems)
@@ -229,7 +233,15 @@ class Executor {
   std::vector<std::vector<char>> gmap_ok_;
   float* d_tap_weights_ = nullptr;                // (kh, kw < 32 / Cin, ci) copies of the stem weights
   long total_slots_ = 0;
-  bool split_ = true;
+  int prec_ = 1;  // 0 tf32, 1 tf32x2, 2 bf16 (ConvParams::prec)
+  // BF16 precision: bf16 copies of the weight pools and their tensor maps
+  // (built on the first set_precision("bf16")).
+  void build_bf16();
+  bool bf16_ready_ = false;
+  std::uint16_t* d_weights_bf16_ = nullptr;
+  std::uint16_t* d_tap_weights_bf16_ = nullptr;
+  std::size_t tap_pool_floats_ = 0;
+  std::vector<std::vector<CUtensorMap>> wmaps_bf_, wmaps_wide_bf_, gmaps_bf_;
   bool stats_on_ = false;
   int stats_every_ = 1;
   long stats_seen_ = 0;

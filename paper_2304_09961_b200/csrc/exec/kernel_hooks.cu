@@ -27,6 +27,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
   float *dwin = nullptr;
   float *din = nullptr, *dw = nullptr, *db = nullptr, *dout = nullptr, *dres = nullptr;
   float** ptrs = nullptr;
+  std::uint16_t* dbf = nullptr;  // bf16 weight copy (d->split == 2)
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   int rc = BS_OK;
 #define CK(x)                                           \
@@ -77,7 +78,9 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     }
     p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_off = d->out_coff;
     p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_off = d->res_coff;
-    p.relu = d->relu; p.round_out = d->round_out; p.split = d->split;
+    p.relu = d->relu; p.round_out = d->round_out; p.prec = d->split;
+    // test hook: force a K split (the executor's autotune sets ks_force per conv)
+    if (const char* ksf = std::getenv("BS_CONV_KS_FORCE")) p.ks_force = std::atoi(ksf);
     WinGeom wg;
     const char* win_env = std::getenv("BS_CONV_WIN");
     if (win_env && win_env[0] == '1' && conv_window_geometry(d->Cin, d->KH, d->KW, d->Ho, d->Wo, d->stride, &wg)) {
@@ -120,6 +123,28 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
         p.tap_rows = 1;
         p.Kpad = d->KH * 32;
         p.wgt = dwin;
+      }
+    }
+    if (d->split == 2) {
+      // BF16: the kernel reads a bf16 copy of the (possibly re-laid) weights.
+      if (p.a_tma) {
+        rc = bs_fail(BS_EINVAL, "bf16 precision runs on the gather path only");
+        goto done;
+      }
+      const int kp = p.tap_rows ? d->KH * 32 : Kpad;
+      CK(cudaMalloc(&dbf, static_cast<size_t>(d->N) * kp * 2));
+      CK(launch_to_bf16(p.tap_rows ? dwin : dw, dbf, static_cast<size_t>(d->N) * kp, 0));
+      if (!encode_weight_map_bf16(&p.wmap, dbf, d->N, kp)) {
+        rc = bs_fail(BS_ECUDA, "bf16 weight map failed");
+        goto done;
+      }
+      if (d->N > 128 && !p.tap_rows) {
+        CUtensorMap wide;
+        if (!encode_weight_map_bf16(&wide, dbf, d->N, kp, 256)) {
+          rc = bs_fail(BS_ECUDA, "bf16 weight map (wide) failed");
+          goto done;
+        }
+        conv_add_wide_map(p, wide);
       }
     }
     unsigned long long* trace = nullptr;
@@ -185,6 +210,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
 done:
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
+  cudaFree(dbf);
   cudaFree(din); cudaFree(dw); cudaFree(dwin); cudaFree(db); cudaFree(dout); cudaFree(dres); cudaFree(ptrs);
   return rc;
 }

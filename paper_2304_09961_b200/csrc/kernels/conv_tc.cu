@@ -28,20 +28,20 @@ int sm_count() {
   return n[dev];
 }
 
-template <int BN, bool SPLIT, bool GROUP>
+template <int BN, int PREC, bool GROUP>
 cudaError_t launch_bn(const ConvParams& p, const ConvParams& p2, int grid, cudaStream_t stream) {
-  using S = conv_tc::Cfg<BN, SPLIT>;
+  using S = conv_tc::Cfg<BN, PREC>;
   static bool configured[kMaxDevices] = {};
   const int dev = current_device();
   if (!configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc::conv_tc_kernel<BN, SPLIT, GROUP>,
+    cudaError_t e = cudaFuncSetAttribute(conv_tc::conv_tc_kernel<BN, PREC, GROUP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     if (e != cudaSuccess) return e;
     configured[dev] = true;
   }
   // Split-K launches are clusters of ksplits CTAs (one per split of a tile).
   const int cluster = p.ksplits > 1 ? p.ksplits : 1;
-  return pdl::launch_ex(conv_tc::conv_tc_kernel<BN, SPLIT, GROUP>, dim3(grid), dim3(S::kThreads), S::kTotal, stream,
+  return pdl::launch_ex(conv_tc::conv_tc_kernel<BN, PREC, GROUP>, dim3(grid), dim3(S::kThreads), S::kTotal, stream,
                         cluster, p, p2);
 }
 
@@ -104,6 +104,19 @@ bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad, int bo
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(w), dims, strides, box,
                                 elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool encode_weight_map_bf16(CUtensorMap* map, const void* w, int N, int Kpad, int box_n) {
+  const EncodeTiledFn encode = encode_fn();
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kpad), static_cast<cuuint64_t>(N)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kpad) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(conv_tc::kBK),
+                             static_cast<cuuint32_t>(box_n > 0 ? box_n : conv_tile_n(N))};
+  const cuuint32_t elem[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box, elem,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool conv_act_geometry(int Cin, int Ho, int Wo, int stride, ActGeom* geom) {
@@ -268,27 +281,23 @@ int choose_ksplits(int tiles, int KT, int sms) {
   return ks;
 }
 
-cudaError_t launch_dispatch(const ConvParams& p, const ConvParams& p2, int bn, int grid, cudaStream_t stream) {
+template <int PREC>
+cudaError_t launch_prec(const ConvParams& p, const ConvParams& p2, int bn, int grid, cudaStream_t stream) {
   if (p.group_units) {  // grouped launches use tile widths <= 128
-    if (p.split) {
-      if (bn == 32) return launch_bn<32, true, true>(p, p2, grid, stream);
-      if (bn == 64) return launch_bn<64, true, true>(p, p2, grid, stream);
-      return launch_bn<128, true, true>(p, p2, grid, stream);
-    }
-    if (bn == 32) return launch_bn<32, false, true>(p, p2, grid, stream);
-    if (bn == 64) return launch_bn<64, false, true>(p, p2, grid, stream);
-    return launch_bn<128, false, true>(p, p2, grid, stream);
+    if (bn == 32) return launch_bn<32, PREC, true>(p, p2, grid, stream);
+    if (bn == 64) return launch_bn<64, PREC, true>(p, p2, grid, stream);
+    return launch_bn<128, PREC, true>(p, p2, grid, stream);
   }
-  if (p.split) {
-    if (bn == 32) return launch_bn<32, true, false>(p, p2, grid, stream);
-    if (bn == 64) return launch_bn<64, true, false>(p, p2, grid, stream);
-    if (bn == 128) return launch_bn<128, true, false>(p, p2, grid, stream);
-    return launch_bn<256, true, false>(p, p2, grid, stream);
-  }
-  if (bn == 32) return launch_bn<32, false, false>(p, p2, grid, stream);
-  if (bn == 64) return launch_bn<64, false, false>(p, p2, grid, stream);
-  if (bn == 128) return launch_bn<128, false, false>(p, p2, grid, stream);
-  return launch_bn<256, false, false>(p, p2, grid, stream);
+  if (bn == 32) return launch_bn<32, PREC, false>(p, p2, grid, stream);
+  if (bn == 64) return launch_bn<64, PREC, false>(p, p2, grid, stream);
+  if (bn == 128) return launch_bn<128, PREC, false>(p, p2, grid, stream);
+  return launch_bn<256, PREC, false>(p, p2, grid, stream);
+}
+
+cudaError_t launch_dispatch(const ConvParams& p, const ConvParams& p2, int bn, int grid, cudaStream_t stream) {
+  if (p.prec == 1) return launch_prec<1>(p, p2, bn, grid, stream);
+  if (p.prec == 2) return launch_prec<2>(p, p2, bn, grid, stream);
+  return launch_prec<0>(p, p2, bn, grid, stream);
 }
 }  // namespace
 
@@ -341,7 +350,7 @@ cudaError_t launch_conv_tc(ConvParams p, cudaStream_t stream) {
 cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream, bool force, int ks) {
   for (const ConvParams* q : {&a, &b})
     if (q->Cin % 4 != 0 || q->Kpad % conv_tc::kBK != 0 || q->Kpad < q->K || q->nimg <= 0 || q->a_tma ||
-        q->a_win || q->tap_rows || q->split != a.split)
+        q->a_win || q->tap_rows || q->prec != a.prec)
       return cudaErrorInvalidValue;
   const int bn = std::max(conv_tile_n(a.N), conv_tile_n(b.N));
   // Unforced, a group is unsplit: decline (the caller launches the two convs

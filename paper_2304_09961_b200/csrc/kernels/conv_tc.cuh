@@ -70,7 +70,7 @@ struct ConvParams {
   int res_ldc;
   int relu;                     // 0 none, 1 ReLU, 2 ReLU6
   int round_out;                // round outputs to TF32 (they feed another GEMM)
-  int split;                    // 1: 2xTF32 (A = A_hi + A_lo, near-fp32 accuracy)
+  int prec;                     // 0 TF32, 1 2xTF32 (A = A_hi + A_lo, near-fp32 accuracy), 2 BF16
   // work decomposition (filled by launch_conv_tc)
   int m_tiles, n_tiles, ksplits;  // K tiles of split s: [s KT / ksplits, (s + 1) KT / ksplits)
   unsigned long long* trace;    // debug timeline of CTA 0 (nullptr in production)
@@ -127,18 +127,21 @@ constexpr int kWinBytes = 65536;  // one input window (window mode); two share t
 // waits on an MMA it does not feed:
 //   raw A  (smem, RA x 16 KB): cp.async gather target; freed as soon as the
 //          converter warps have read a stage (not when the MMA finishes);
-//   B      (smem, NB x BN*128 B): weights by TMA, 128B-swizzled for UMMA;
-//   A op   (TMEM, TA slots): converted A operand, [hi | lo] for 2xTF32;
-//          the MMAs read A from TMEM, so shared memory only serves B to the
-//          tensor core.
-template <int BN, bool SPLIT>
+//   B      (smem, NB x BN*128 B): weights by TMA, 128B-swizzled for UMMA
+//          (bf16: BN*64 B stages, 64B-swizzled);
+//   A op   (TMEM, TA slots): converted A operand, [hi | lo] for 2xTF32,
+//          packed bf16 pairs for BF16; the MMAs read A from TMEM, so shared
+//          memory only serves B to the tensor core.
+// PREC: 0 = TF32 (one MMA), 1 = 2xTF32 (split A, ~fp32 accuracy),
+//       2 = BF16 (A rounded to bf16 by the converters, bf16 weights).
+template <int BN, int PREC>
 struct Cfg {
   static constexpr int kThreads = 608;
   // BN = 256: one accumulator (256 columns) so the A slots still fit in TMEM;
   // the raw A ring shrinks to make room for the 32 KB B stages.
   static constexpr int kAcc = BN == 256 ? 1 : 2;                 // TMEM accumulator buffers
   static constexpr int RA = BN == 32 ? 10 : BN == 256 ? 6 : 8;
-  static constexpr int kACols = SPLIT ? 2 * kBK : kBK;          // TMEM columns per A slot
+  static constexpr int kACols = PREC == 1 ? 2 * kBK : PREC == 2 ? kBK / 2 : kBK;  // TMEM columns per A slot
   static constexpr int kTA0 = kAcc * BN;                         // first A column (after the accumulators)
   // One operand stage = (TMEM A slot, B smem stage), released by a single
   // tcgen05.commit per K tile (each commit costs the tensor pipe ~84 cycles).
@@ -146,11 +149,12 @@ struct Cfg {
   // Per epilogue warp: bias [2][BN] fp32, blob-table entries [2][32] (out,
   // residual) and the unit's final row pointers [32] (out, residual).
   static constexpr int kEpiWarpBytes = 8 * BN + 1536;
-  static constexpr int kNBmax = (232448 - 1024 - 512 - RA * kBM * 128 - kBM * 32 * 4 - 4 * kEpiWarpBytes) / (BN * 128);
+  static constexpr int kBRow = PREC == 2 ? 64 : 128;             // bytes per weight row of a K tile
+  static constexpr int kNBmax = (232448 - 1024 - 512 - RA * kBM * 128 - kBM * 32 * 4 - 4 * kEpiWarpBytes) / (BN * kBRow);
   static constexpr int TA = kTAmax < kNBmax ? (kTAmax < 8 ? kTAmax : 8) : (kNBmax < 8 ? kNBmax : 8);
   static constexpr int NB = TA;
   static constexpr int kABytes = kBM * 128;
-  static constexpr int kBBytes = BN * 128;
+  static constexpr int kBBytes = BN * kBRow;
   static constexpr int kBOffset = RA * kABytes;
   static constexpr int kStagingOffset = kBOffset + NB * kBBytes;  // epilogue staging, 128 x 32 fp32
   static constexpr int kEpiOffset = kStagingOffset + kBM * 32 * 4;
@@ -237,6 +241,32 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
   }
 }
 
+// One K-tile row of A (32 fp32 values, this thread's TMEM lane) -> operand
+// registers: TF32 / 2xTF32 hi (+ lo) words, or (BF16) 16 packed bf16 pairs.
+template <int PREC>
+__device__ __forceinline__ void a_operand(const float4 (&v)[8], uint32_t (&hi)[32], uint32_t (&lo)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if constexpr (PREC == 2) {
+      hi[2 * c] = ptx::pack_bf16x2(v[c].x, v[c].y);
+      hi[2 * c + 1] = ptx::pack_bf16x2(v[c].z, v[c].w);
+    } else {
+      const float x[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) split_tf32<PREC == 1>(x[e], hi[4 * c + e], lo[4 * c + e]);
+    }
+  }
+}
+template <int PREC>
+__device__ __forceinline__ void a_store(uint32_t dst, const uint32_t (&hi)[32], const uint32_t (&lo)[32]) {
+  if constexpr (PREC == 2) {
+    ptx::tmem_st16(dst, *reinterpret_cast<const uint32_t(*)[16]>(hi));
+  } else {
+    ptx::tmem_st32(dst, hi);
+    if constexpr (PREC == 1) ptx::tmem_st32(dst + kBK, lo);
+  }
+}
+
 __device__ __forceinline__ float epilogue_op(const ConvParams& p, float x, int n, const float* res_row) {
   if (p.bias) x += __ldg(p.bias + n);
   if (res_row) x += res_row[n];
@@ -246,13 +276,14 @@ __device__ __forceinline__ float epilogue_op(const ConvParams& p, float x, int n
   return x;
 }
 
-template <int BN, bool SPLIT, bool GROUP>
-__global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
+template <int BN, int PREC, bool GROUP>
+__global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p_a, const __grid_constant__ ConvParams p_b) {
   // Roles take the problem of each unit from BS_UNIT_PROBLEM (p_a for the
   // first units0 units, p_b after); outside unit loops p is p_a.
   const ConvParams& p = p_a;
-  using S = Cfg<BN, SPLIT>;
+  using S = Cfg<BN, PREC>;
+  constexpr bool SPLIT = PREC == 1, BF16 = PREC == 2;
   constexpr int RA = S::RA, NB = S::NB, TA = S::TA;
   extern __shared__ uint8_t smem_raw[];
   // Align by pointer arithmetic on the __shared__ array (not via uintptr_t)
@@ -408,12 +439,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           }
           uint32_t hi[32];
           [[maybe_unused]] uint32_t lo[32];
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            const float x[4] = {v[cc].x, v[cc].y, v[cc].z, v[cc].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) split_tf32<SPLIT>(x[e], hi[4 * cc + e], lo[4 * cc + e]);
-          }
+          a_operand<PREC>(v, hi, lo);
           const int sa = it % TA;
           const bool tr = p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48;
           if (tr) p.trace[2048 + it * 4 + 0] = gtime();
@@ -421,8 +447,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
           if (tr) p.trace[2048 + it * 4 + 1] = gtime();
           ptx::tc_fence_after();
           const uint32_t dst = lane_base + sa * S::kACols;
-          ptx::tmem_st32(dst, hi);
-          if constexpr (SPLIT) ptx::tmem_st32(dst + kBK, lo);
+          a_store<PREC>(dst, hi, lo);
           if (tr) p.trace[2048 + it * 4 + 2] = gtime();
           ptx::tmem_st_wait();
           if (tr) p.trace[2048 + it * 4 + 3] = gtime();
@@ -479,19 +504,13 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
         ptx::mbar_arrive(&ra_empty[s]);
         uint32_t hi[32];
         [[maybe_unused]] uint32_t lo[32];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float x[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) split_tf32<SPLIT>(x[e], hi[4 * c + e], lo[4 * c + e]);
-        }
+        a_operand<PREC>(v, hi, lo);
         const int sa = it % TA;
         if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t dst = lane_base + sa * S::kACols;
         if (!(p.debug & 1)) {
-          ptx::tmem_st32(dst, hi);
-          if constexpr (SPLIT) ptx::tmem_st32(dst + kBK, lo);
+          a_store<PREC>(dst, hi, lo);
           ptx::tmem_st_wait();
         }
         ptx::tc_fence_before();
@@ -1029,7 +1048,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
     }
   } else if (warp == 8) {
     // ---------------------------------------------------------- MMA issue
-    constexpr uint32_t idesc = ptx::make_idesc(2, kBM, BN);
+    constexpr uint32_t idesc = ptx::make_idesc(BF16 ? 1 : 2, kBM, BN);
     const uint32_t a_tmem0 = tmem_base + S::kTA0;
     int it = 0, j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
@@ -1047,13 +1066,22 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::kThreads, 1)
         if (p.trace && lane == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 4] = gtime();
         if (ptx::elect_one()) {
           const uint32_t a_slot = a_tmem0 + sa * S::kACols;
-          const uint64_t b_desc = ptx::sw128_kmajor_desc(smem_base + S::kBOffset + sb * S::kBBytes);
+          const uint32_t b_addr = smem_base + S::kBOffset + sb * S::kBBytes;
+          if constexpr (BF16) {
+            // K = 16 bf16 per MMA: A 8 TMEM columns, B +32 bytes in the 64-byte row.
+            const uint64_t b_desc = ptx::sw64_kmajor_desc(b_addr);
 #pragma unroll
-          for (int k = 0; k < kBK / 8; ++k) {
-            // A: 8 TMEM columns per K=8 step; B: +32 bytes inside the swizzled row.
-            ptx::mma_tf32_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
-            if constexpr (SPLIT)
-              if (!(p.debug & 2)) ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
+            for (int k = 0; k < kBK / 16; ++k)
+              ptx::mma_bf16_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
+          } else {
+            const uint64_t b_desc = ptx::sw128_kmajor_desc(b_addr);
+#pragma unroll
+            for (int k = 0; k < kBK / 8; ++k) {
+              // A: 8 TMEM columns per K=8 step; B: +32 bytes inside the swizzled row.
+              ptx::mma_tf32_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
+              if constexpr (SPLIT)
+                if (!(p.debug & 2)) ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
+            }
           }
           ptx::mma_commit(&ta_empty[sa]);  // == b_empty[sb]
           if (kt == w.kt1 - 1) ptx::mma_commit(&acc_full[acc]);
@@ -1183,6 +1211,9 @@ void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& geom
                       long slot_floats, long slots);
 // Encodes a weight tensor map for w ([N][Kpad] floats) and the tile conv_tile_n(N).
 bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad, int box_n = 0);
+// The same for a bf16 copy of the weights (BF16 precision): box {32, BN},
+// 64-byte swizzle.
+bool encode_weight_map_bf16(CUtensorMap* map, const void* w_bf16, int N, int Kpad, int box_n = 0);
 // Offers the launcher 128 x 256 tiles (weights map with box_n = 256).
 void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide);
 // Grouped launch of two independent convs (no data flow between them; same

@@ -5,6 +5,9 @@
 #include "ptx.cuh"
 #include "simple_ops.cuh"
 
+#include <cuda_bf16.h>
+#include <algorithm>
+
 namespace bs200 {
 
 namespace {
@@ -469,7 +472,20 @@ __global__ void expand_rgb_kernel(const float* __restrict__ rgb, float* __restri
   }
 }
 
+__global__ void to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, std::size_t n) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
 }  // namespace
+
+cudaError_t launch_to_bf16(const float* src, std::uint16_t* dst, std::size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>(std::min<std::size_t>((n + 255) / 256, 148 * 16));
+  to_bf16_kernel<<<blocks, 256, 0, s>>>(src, reinterpret_cast<__nv_bfloat16*>(dst), n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_expand_rgb(const float* rgb, float* dst, int hw, cudaStream_t s) {
   cudaError_t e = cudaSuccess;

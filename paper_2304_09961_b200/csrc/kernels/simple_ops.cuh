@@ -4,6 +4,8 @@
 // tensor-core conv. Channels are processed four at a time (float4) so warps
 // issue 512-byte coalesced requests along the channel axis.
 #pragma once
+#include <cstddef>
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace bs200 {
@@ -66,5 +68,7 @@ struct GatherParams {
   int n, cnt;
 };
 cudaError_t launch_gather_out(const GatherParams& p, cudaStream_t s);
+// dst[i] = bf16 round-to-nearest-even of src[i] (weight copies for BF16 precision).
+cudaError_t launch_to_bf16(const float* src, std::uint16_t* dst, std::size_t n, cudaStream_t s);
 
 }  // namespace bs200

@@ -312,3 +312,49 @@ def test_tile_autotune_keeps_parity():
         for i in ids:
             p = ex.retire(i, 1000)
             assert_request_matches(p, refs[i % 3], TOL)
+
+
+def bf16_report(suite, n_images=48, seed=7):
+    """BF16 path (reported separately, north_star): one full-network step of
+    n_images requests in bf16 precision against the fp32 CPU forward
+    (oracle/torch_forward.py, batched torch.nn.functional on the same
+    weights). Returns max |logit error| / max |logit| over the batch, the
+    median per-request error and the top-1 agreement rate."""
+    import torch
+
+    from oracle.torch_forward import TorchNet
+    from paper_2304_09961_b200.executor import Executor
+    with Executor(suite, max_batch=90, max_requests=n_images + 2) as ex:
+        ex.set_precision("bf16")
+        net = ex.desc["nets"][0]
+        imgs = np.stack([image_for(ex, 0, i, seed) for i in range(n_images)])
+        for i in range(n_images):
+            ex.admit(i + 1, 0, imgs[i])
+        ex.plan(1)
+        ex.step(1, 0, 0, 1, len(net["layers"]), [(i + 1, 1) for i in range(n_images)])
+        got = np.stack([ex.retire(i + 1, net["classes"], logits=True) for i in range(n_images)])
+        w = ex.weights()
+        ref, _ = TorchNet(ex.desc, 0, w, dtype=torch.float64).forward(imgs)
+        emu, _ = TorchNet(ex.desc, 0, w, dtype=torch.float64, bf16_convs=True).forward(imgs)
+    per = np.abs(got - ref).max(axis=1) / np.abs(ref).max(axis=1)
+    top1 = float(np.mean(np.argmax(got, 1) == np.argmax(ref, 1)))
+    return {"err_vs_fp32": float(np.abs(got - ref).max() / np.abs(ref).max()),
+            "median_err_vs_fp32": float(np.median(per)), "top1_agreement_vs_fp32": top1,
+            "err_vs_bf16_emulation": float(np.abs(got - emu).max() / np.abs(emu).max()),
+            "top1_agreement_vs_bf16_emulation": float(np.mean(np.argmax(got, 1) == np.argmax(emu, 1))),
+            "emulation_err_vs_fp32": float(np.abs(emu - ref).max() / np.abs(ref).max())}
+
+
+@pytest.mark.parametrize("suite", ["googlenet", "resnet50", "mobilenet_v2"])
+def test_bf16_path_tolerance_and_top1(suite):
+    """bf16 is reported separately from the fp32 bar (figures printed; DESIGN
+    §5). Per conv the kernel is exact for bf16 operands
+    (test_kernels_gpu.py::test_conv_bf16_operands, 2e-5); end to end, a
+    one-ulp difference in an accumulation order flips later bf16 roundings,
+    so the GPU is checked to track a CPU emulation of the same rounding
+    closer than bf16 itself tracks fp32, with the emulation's top-1."""
+    r = bf16_report(suite)
+    print(f"{suite} bf16: " + ", ".join(f"{k} {v:.4g}" for k, v in r.items()))
+    assert r["err_vs_bf16_emulation"] < 0.75 * r["emulation_err_vs_fp32"]
+    assert r["top1_agreement_vs_bf16_emulation"] >= 0.9
+    assert r["err_vs_fp32"] < 0.25

@@ -14,7 +14,12 @@ TOL = 2e-5
 
 
 def run_conv(nimg, H, W, Cin, N, KH, KW, stride, pad, *, in_ldc=None, in_coff=0, out_ldc=None,
-             out_coff=0, residual=False, relu=0, bias=True, seed=0, round_out=0, split=0, raw_input=False):
+             out_coff=0, residual=False, relu=0, bias=True, seed=0, round_out=0, split=0, raw_input=False,
+             bf16_ref=False):
+    """Runs the conv kernel through the C-ABI test hook; returns max|gpu - ref|
+    / max|ref|. split: 0 TF32, 1 2xTF32, 2 BF16. bf16_ref: the reference sees
+    the operands rounded to bf16 (what the BF16 path multiplies), so only the
+    fp32 accumulation order differs."""
     from paper_2304_09961_b200._native import bs_conv_desc, check, exec_lib, fptr
     rng = np.random.default_rng(seed)
     in_ldc = in_ldc or Cin
@@ -34,7 +39,11 @@ def run_conv(nimg, H, W, Cin, N, KH, KW, stride, pad, *, in_ldc=None, in_coff=0,
     res_full = rng.standard_normal((nimg, Ho, Wo, out_ldc)).astype(np.float32) if residual else None
     out = np.full((nimg, Ho, Wo, out_ldc), 7.0, np.float32)
 
-    ref = conv2d_nhwc(x, w, b, stride, pad)
+    if bf16_ref:
+        from oracle.layers import round_bf16
+        ref = conv2d_nhwc(round_bf16(x), round_bf16(w), b, stride, pad)
+    else:
+        ref = conv2d_nhwc(x, w, b, stride, pad)
     if residual:
         ref = ref + res_full[..., out_coff:out_coff + N]
     if relu == 1:
@@ -120,6 +129,29 @@ def test_conv_large_batch():
 def test_conv_split_tf32x2_full_fp32_inputs(case):
     """2xTF32: un-rounded fp32 activations, TF32 weights -> fp32-level error."""
     assert run_conv(**case, split=1, raw_input=True) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES[:10] + CASES[15:], ids=lambda c: "x".join(str(c[k]) for k in ("nimg", "H", "Cin", "N", "KH", "stride")))
+def test_conv_bf16_operands(case):
+    """BF16 precision (kind::f16 MMAs, A rounded to bf16 by the converters,
+    bf16 weight copies by 64B-swizzled TMA): exact bf16 products with fp32
+    accumulation -- 2e-5 against a reference on bf16-rounded operands, and
+    within bf16 rounding (1e-2) of the fp32 result."""
+    assert run_conv(**case, split=2, raw_input=True, bf16_ref=True) < TOL
+    assert run_conv(**case, split=2, raw_input=True) < 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split", [1, 2])
+def test_conv_cluster_split_k_forced(split, monkeypatch):
+    """Every K split the autotune may force (cluster of 2..8 CTAs per tile,
+    DSMEM reduction), including ragged K tiles per split."""
+    for ks in ("2", "3", "5", "8"):
+        monkeypatch.setenv("BS_CONV_KS_FORCE", ks)
+        assert run_conv(1, 7, 7, 832, 384, 1, 1, 1, 0, split=split, raw_input=True,
+                        bf16_ref=split == 2, residual=True, relu=1) < TOL
+        assert run_conv(3, 14, 14, 96, 208, 3, 3, 1, 1, split=split, raw_input=True, bf16_ref=split == 2) < TOL
 
 
 @pytest.mark.gpu
