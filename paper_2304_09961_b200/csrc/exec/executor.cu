@@ -102,47 +102,6 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
         throw std::runtime_error("cuTensorMapEncodeTiled (wide) failed for " + op.name);
     }
   }
-  // Window mode for spatial convs (opt-in, BS_CONV_WIN=1; measured slower
-  // than the cp.async gather on B200): the
-  // weights are re-laid chunk-major into their own pool, and each conv gets a
-  // window tensor map over the slot space.
-  const char* win_env = std::getenv("BS_CONV_WIN");
-  const bool use_win = win_env && win_env[0] == '1';
-  wins_.resize(suite_.nets.size());
-  {
-    std::vector<float> pool;
-    std::vector<std::pair<std::size_t, std::size_t>> where;  // (net, op) of each window conv
-    for (std::size_t n = 0; n < suite_.nets.size() && use_win; ++n) {
-      const NetDef& net = suite_.nets[n];
-      wins_[n].resize(net.ops.size());
-      for (std::size_t i = 0; i < net.ops.size(); ++i) {
-        const OpDef& op = net.ops[i];
-        if (op.kind != OpKind::conv) continue;
-        WinMap& wm = wins_[n][i];
-        if (!conv_window_geometry(op.in.C, op.KH, op.KW, op.Ho, op.Wo, op.stride, &wm.geom)) continue;
-        wm.w_off = pool.size();
-        pool.resize(pool.size() + static_cast<std::size_t>(op.out.C) * wm.geom.Kwin);
-        conv_window_weights(suite_.weights.data() + op.w_off, op.out.C, op.Kpad, op.KH, op.KW, op.in.C, wm.geom,
-                            pool.data() + wm.w_off);
-        where.emplace_back(n, i);
-      }
-    }
-    if (!pool.empty()) {
-      ck(cudaMalloc(&d_win_weights_, pool.size() * sizeof(float)), "window weights");
-      ck(cudaMemcpy(d_win_weights_, pool.data(), pool.size() * sizeof(float), cudaMemcpyHostToDevice),
-         "window weights H2D");
-    }
-    for (const auto& [n, i] : where) {
-      const NetDef& net = suite_.nets[n];
-      const OpDef& op = net.ops[i];
-      const TensorDef& ti = net.tensors[static_cast<std::size_t>(op.in.t)];
-      WinMap& wm = wins_[n][i];
-      wm.ok = encode_weight_map(&wm.wmap, d_win_weights_ + wm.w_off, op.out.C, wm.geom.Kwin) &&
-              encode_window_map(&wm.amap, arena_ + ti.off + op.in.coff, op.in.C, ti.W, ti.H, ti.C, total_slots_,
-                                static_cast<long>(slot_floats_), wm.geom);
-      if (!wm.ok) throw std::runtime_error("window tensor maps failed for " + op.name);
-    }
-  }
   // Tap-row mode for the stems (default; BS_CONV_TAPROW=0 disables): one K
   // tile per filter row, so the A gather is one contiguous 128-byte segment
   // per output pixel and K tile. Weights re-laid to match.
@@ -158,7 +117,6 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
       for (std::size_t i = 0; i < net.ops.size(); ++i) {
         const OpDef& op = net.ops[i];
         if (op.kind != OpKind::conv || op.out.C > 128 || !conv_tap_rows_eligible(op.in.C, op.KW)) continue;
-        if (n < wins_.size() && i < wins_[n].size() && wins_[n][i].ok) continue;
         TapRowMap& tm = taps_[n][i];
         tm.w_off = pool.size();
         pool.resize(pool.size() + static_cast<std::size_t>(op.out.C) * op.KH * 32);
@@ -178,26 +136,6 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
       TapRowMap& tm = taps_[n][i];
       tm.ok = encode_weight_map(&tm.wmap, d_tap_weights_ + tm.w_off, op.out.C, op.KH * 32);
       if (!tm.ok) throw std::runtime_error("tap-row weight map failed for " + op.name);
-    }
-  }
-  // One activation tensor map per conv input (the slot space never moves).
-  // BS_CONV_TMA=1: feed conv activations by TMA boxes wherever the geometry
-  // allows (default: cp.async gather; see DESIGN.md §4 for the ingest limits).
-  const char* tma_env = std::getenv("BS_CONV_TMA");
-  const bool no_tma = !(tma_env && tma_env[0] == '1');
-  amaps_.resize(suite_.nets.size());
-  for (std::size_t n = 0; n < suite_.nets.size() && !no_tma; ++n) {
-    const NetDef& net = suite_.nets[n];
-    amaps_[n].resize(net.ops.size());
-    for (std::size_t i = 0; i < net.ops.size(); ++i) {
-      const OpDef& op = net.ops[i];
-      if (op.kind != OpKind::conv) continue;
-      const TensorDef& ti = net.tensors[static_cast<std::size_t>(op.in.t)];
-      ActMap& am = amaps_[n][i];
-      if (!conv_act_geometry(op.in.C, op.Ho, op.Wo, op.stride, &am.geom)) continue;
-      am.ok = encode_act_map(&am.map, arena_ + ti.off + op.in.coff, op.in.C, ti.W, ti.H, ti.C, total_slots_,
-                             static_cast<long>(slot_floats_), am.geom, op.stride);
-      if (!am.ok) throw std::runtime_error("activation tensor map failed for " + op.name);
     }
   }
   plan_groups();
@@ -234,9 +172,7 @@ void Executor::plan_groups() {
     auto groupable = [&](int i) {
       const OpDef& op = net.ops[static_cast<std::size_t>(i)];
       const auto k = static_cast<std::size_t>(i);
-      return op.kind == OpKind::conv && !(n < taps_.size() && k < taps_[n].size() && taps_[n][k].ok) &&
-             !(n < wins_.size() && k < wins_[n].size() && wins_[n][k].ok) &&
-             !(n < amaps_.size() && k < amaps_[n].size() && amaps_[n][k].ok);
+      return op.kind == OpKind::conv && !(n < taps_.size() && k < taps_[n].size() && taps_[n][k].ok);
     };
     for (const LayerDef& L : net.layers) {
       std::vector<LayerItem> items;
@@ -299,7 +235,6 @@ Executor::~Executor() {
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (float* p : pool_) cudaFree(p);
   cudaFree(d_weights_);
-  cudaFree(d_win_weights_);
   cudaFree(d_tap_weights_);
   cudaFree(d_weights_bf16_);
   cudaFree(d_tap_weights_bf16_);
@@ -447,15 +382,7 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
   {
     const std::size_t ni = static_cast<std::size_t>(&net - suite_.nets.data());
     const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
-    if (bf) {
-      // BF16: cp.async gather (+ tap rows); the opt-in TMA activation modes are fp32 only
-    } else if (ni < wins_.size() && oi < wins_[ni].size() && wins_[ni][oi].ok)
-      conv_use_window(p, wins_[ni][oi].amap, wins_[ni][oi].wmap, wins_[ni][oi].geom, arena_,
-                      static_cast<long>(slot_floats_), total_slots_);
-    else if (ni < amaps_.size() && oi < amaps_[ni].size() && amaps_[ni][oi].ok)
-      conv_use_act_map(p, amaps_[ni][oi].map, amaps_[ni][oi].geom, arena_, static_cast<long>(slot_floats_),
-                       total_slots_);
-    if (ni < taps_.size() && oi < taps_[ni].size() && taps_[ni][oi].ok && !p.a_tma) {
+    if (ni < taps_.size() && oi < taps_[ni].size() && taps_[ni][oi].ok) {
       p.tap_rows = 1;
       p.Kpad = op.KH * 32;
       p.wmap = bf ? taps_[ni][oi].wmap_bf : taps_[ni][oi].wmap;

@@ -202,20 +202,6 @@ class Executor {
   std::vector<int> pool_n_;
   std::vector<std::vector<CUtensorMap>> wmaps_;  // [net][op] weight tensor maps
   std::vector<std::vector<CUtensorMap>> wmaps_wide_;  // [net][op] 256-row boxes (N > 128)
-  struct ActMap {
-    CUtensorMap map{};
-    ActGeom geom;
-    bool ok = false;
-  };
-  std::vector<std::vector<ActMap>> amaps_;        // [net][op] conv input maps over the slot space
-  struct WinMap {
-    CUtensorMap amap{}, wmap{};
-    WinGeom geom;
-    std::size_t w_off = 0;  // into d_win_weights_
-    bool ok = false;
-  };
-  std::vector<std::vector<WinMap>> wins_;         // [net][op] window-mode maps (spatial convs)
-  float* d_win_weights_ = nullptr;                // chunk-major copies of the spatial conv weights
   struct TapRowMap {
     bool ok = false;
     CUtensorMap wmap{};

@@ -28,6 +28,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
   float *din = nullptr, *dw = nullptr, *db = nullptr, *dout = nullptr, *dres = nullptr;
   float** ptrs = nullptr;
   std::uint16_t* dbf = nullptr;  // bf16 weight copy (d->split == 2)
+  CUtensorMap wide;              // 256-row weight box (the launcher keeps a pointer)
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   int rc = BS_OK;
 #define CK(x)                                           \
@@ -69,7 +70,6 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
       goto done;
     }
     if (d->N > 128) {
-      CUtensorMap wide;
       if (!encode_weight_map(&wide, dw, d->N, Kpad, 256)) {
         rc = bs_fail(BS_ECUDA, "cuTensorMapEncodeTiled (wide) failed");
         goto done;
@@ -81,36 +81,9 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     p.relu = d->relu; p.round_out = d->round_out; p.prec = d->split;
     // test hook: force a K split (the executor's autotune sets ks_force per conv)
     if (const char* ksf = std::getenv("BS_CONV_KS_FORCE")) p.ks_force = std::atoi(ksf);
-    WinGeom wg;
-    const char* win_env = std::getenv("BS_CONV_WIN");
-    if (win_env && win_env[0] == '1' && conv_window_geometry(d->Cin, d->KH, d->KW, d->Ho, d->Wo, d->stride, &wg)) {
-      // Window mode: chunk-major weights + window map over the nimg images.
-      std::vector<float> hw(static_cast<size_t>(d->N) * wg.Kwin);
-      conv_window_weights(w_host, d->N, Kpad, d->KH, d->KW, d->Cin, wg, hw.data());
-      CK(cudaMalloc(&dwin, hw.size() * sizeof(float)));
-      CK(cudaMemcpy(dwin, hw.data(), hw.size() * sizeof(float), cudaMemcpyHostToDevice));
-      CUtensorMap amap, wmap;
-      if (!encode_window_map(&amap, din + d->in_coff, d->Cin, d->W, d->H, d->in_ldc, nimg, static_cast<long>(in_img),
-                             wg) ||
-          !encode_weight_map(&wmap, dwin, d->N, wg.Kwin)) {
-        rc = bs_fail(BS_ECUDA, "window tensor maps failed");
-        goto done;
-      }
-      conv_use_window(p, amap, wmap, wg, din, static_cast<long>(in_img), nimg);
-    } else {
-      // TMA activation path: the nimg input images are the slot space.
-      ActGeom g;
-      CUtensorMap amap;
-      const char* tma_env = std::getenv("BS_CONV_TMA");
-      if (tma_env && tma_env[0] == '1' && conv_act_geometry(d->Cin, d->Ho, d->Wo, d->stride, &g)) {
-        if (!encode_act_map(&amap, din + d->in_coff, d->Cin, d->W, d->H, d->in_ldc, nimg,
-                            static_cast<long>(in_img), g, d->stride)) {
-          rc = bs_fail(BS_ECUDA, "activation tensor map failed");
-          goto done;
-        }
-        conv_use_act_map(p, amap, g, din, static_cast<long>(in_img), nimg);
-      } else if (d->N <= 128 && conv_tap_rows_eligible(d->Cin, d->KW) &&
-                 !(std::getenv("BS_CONV_TAPROW") && std::getenv("BS_CONV_TAPROW")[0] == '0')) {
+    {
+      if (d->N <= 128 && conv_tap_rows_eligible(d->Cin, d->KW) &&
+          !(std::getenv("BS_CONV_TAPROW") && std::getenv("BS_CONV_TAPROW")[0] == '0')) {
         // Tap-row mode (the executor's rule for the stems): re-laid weights.
         std::vector<float> hw(static_cast<size_t>(d->N) * d->KH * 32);
         conv_tap_row_weights(w_host, d->N, Kpad, d->KH, d->KW, d->Cin, hw.data());
@@ -127,10 +100,6 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
     }
     if (d->split == 2) {
       // BF16: the kernel reads a bf16 copy of the (possibly re-laid) weights.
-      if (p.a_tma) {
-        rc = bs_fail(BS_EINVAL, "bf16 precision runs on the gather path only");
-        goto done;
-      }
       const int kp = p.tap_rows ? d->KH * 32 : Kpad;
       CK(cudaMalloc(&dbf, static_cast<size_t>(d->N) * kp * 2));
       CK(launch_to_bf16(p.tap_rows ? dwin : dw, dbf, static_cast<size_t>(d->N) * kp, 0));
@@ -139,7 +108,6 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
         goto done;
       }
       if (d->N > 128 && !p.tap_rows) {
-        CUtensorMap wide;
         if (!encode_weight_map_bf16(&wide, dbf, d->N, kp, 256)) {
           rc = bs_fail(BS_ECUDA, "bf16 weight map (wide) failed");
           goto done;

@@ -87,6 +87,9 @@ json serve_live(Executor& ex, const json& j) {
 
   const std::vector<ArrivalRecord> arrivals = generate_arrivals(job.spec);
   const std::size_t n = arrivals.size();
+  // ids follow arrival order (the pending queue's binary search relies on it)
+  for (std::size_t i = 1; i < n; ++i)
+    if (arrivals[i].time < arrivals[i - 1].time) throw std::logic_error("serve: arrivals out of time order");
   std::vector<Book> book(n);
   std::vector<int> mix;
   if (job.spec.dnn_mix.empty()) {
@@ -200,13 +203,20 @@ json serve_live(Executor& ex, const json& j) {
         const auto hs0 = Clock::now();
         const detail::ExecStep st = steps[next_step];
         const ScheduledSegment& seg = plan.segments[static_cast<std::size_t>(st.segment)];
+        // pending is FIFO by (arrival, id) and live ids are assigned in
+        // arrival order, so it is sorted by id: members are found by binary
+        // search (was a linear scan of pending per member).
+        auto find_pending = [&](RequestId id) {
+          auto it = std::lower_bound(pending.begin(), pending.end(), id,
+                                     [](const Request& r, RequestId v) { return r.id < v; });
+          return (it != pending.end() && it->id == id) ? it : pending.end();
+        };
         std::vector<std::pair<std::int64_t, int>> members;
-        for (RequestId id : seg.members)
-          for (const Request& r : pending)
-            if (r.id == id) {
-              members.emplace_back(id, r.layer);
-              break;
-            }
+        members.reserve(seg.members.size());
+        for (RequestId id : seg.members) {
+          auto it = find_pending(id);
+          if (it != pending.end()) members.emplace_back(id, it->layer);
+        }
         ex.step(plan_no, st.segment, dnn_map[static_cast<std::size_t>(seg.dnn)], st.layer_from, st.layer_to, members,
                 seg.riders);
         ++n_steps;
@@ -216,7 +226,7 @@ json serve_live(Executor& ex, const json& j) {
         InFlight f;
         bool crossed = false;
         for (RequestId id : seg.members) {
-          auto it = std::find_if(pending.begin(), pending.end(), [id](const Request& r) { return r.id == id; });
+          auto it = find_pending(id);
           if (it == pending.end() || it->layer > st.layer_to) continue;
           const int was = it->layer;
           it->layer = st.layer_to + 1;
@@ -232,7 +242,7 @@ json serve_live(Executor& ex, const json& j) {
         std::vector<std::int64_t> deposited;
         for (const Rider& rider : seg.riders) {
           if (rider.leave_layer > st.layer_to || rider.join_layer > st.layer_to) continue;
-          auto it = std::find_if(pending.begin(), pending.end(), [&](const Request& r) { return r.id == rider.id; });
+          auto it = find_pending(rider.id);
           if (it == pending.end() || it->dnn != rider.dnn || it->layer >= rider.deposit_layer) continue;
           it->layer = rider.deposit_layer;
           crossed = true;
@@ -240,7 +250,7 @@ json serve_live(Executor& ex, const json& j) {
         }
         ex.step_done(deposited);
         for (std::int64_t id : deposited) {
-          auto it = std::find_if(pending.begin(), pending.end(), [id](const Request& r) { return r.id == id; });
+          auto it = find_pending(id);
           if (it != pending.end() && it->layer > job.ps.dnns[static_cast<std::size_t>(it->dnn)].num_layers()) {
             d2h_bytes += classes * static_cast<long>(sizeof(float));
             f.finishing.push_back(id);

@@ -41,8 +41,11 @@ cudaError_t launch_bn(const ConvParams& p, const ConvParams& p2, int grid, cudaS
   }
   // Split-K launches are clusters of ksplits CTAs (one per split of a tile).
   const int cluster = p.ksplits > 1 ? p.ksplits : 1;
+  conv_tc::ConvArgs<GROUP> args;
+  args.a = p;
+  if constexpr (GROUP) args.b = p2;
   return pdl::launch_ex(conv_tc::conv_tc_kernel<BN, PREC, GROUP>, dim3(grid), dim3(S::kThreads), S::kTotal, stream,
-                        cluster, p, p2);
+                        cluster, args);
 }
 
 }  // namespace
@@ -59,7 +62,7 @@ namespace {
 // GPU. BS_CONV_BN256=0 disables, =2 forces (when a wide weight map exists).
 bool use_wide(const ConvParams& p, int sms) {
   const char* env = std::getenv("BS_CONV_BN256");  // read per launch (tests toggle it)
-  if (!p.has_wide || p.a_win || (env && env[0] == '0')) return false;
+  if (!p.wmap_wide || (env && env[0] == '0')) return false;
   if (env && env[0] == '2') return true;
   if (p.wide_pref == 1) return true;
   if (p.wide_pref == 2) return false;
@@ -68,11 +71,7 @@ bool use_wide(const ConvParams& p, int sms) {
 }
 }  // namespace
 
-void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide) {
-  p.wmap_wide = wide;
-  p.has_wide = 1;
-}
-
+void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide) { p.wmap_wide = &wide; }
 
 namespace {
 // The driver entry point is resolved through the runtime, so the library has
@@ -119,74 +118,6 @@ bool encode_weight_map_bf16(CUtensorMap* map, const void* w, int N, int Kpad, in
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool conv_act_geometry(int Cin, int Ho, int Wo, int stride, ActGeom* geom) {
-  if (Ho <= 0 || Wo <= 0 || Wo > 128 || stride < 1 || stride > 2) return false;
-  ActGeom g;
-  g.Wb = 1;
-  while (g.Wb < Wo) g.Wb *= 2;
-  int hp = 1;
-  while (hp < Ho) hp *= 2;
-  g.Hb = std::min(conv_tc::kBM / g.Wb, hp);
-  const int R = g.Wb * g.Hb;
-  if (R < 32 || conv_tc::kBM % R != 0) return false;
-  g.G = conv_tc::kBM / R;
-  g.tpi = (Ho + g.Hb - 1) / g.Hb;
-  if (g.G > 1 && g.tpi != 1) return false;
-  if (g.Wb * stride > 256 || g.Hb * stride > 256) return false;
-  g.g = Cin % 32 == 0 ? 32 : Cin % 16 == 0 ? 16 : Cin % 8 == 0 ? 8 : Cin % 4 == 0 ? 4 : 0;
-  if (!g.g) return false;
-  *geom = g;
-  return true;
-}
-
-bool encode_act_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
-                    long slot_floats, const ActGeom& g, int stride) {
-  const EncodeTiledFn encode = encode_fn();
-  if (!encode || (reinterpret_cast<uintptr_t>(base) & 15) || ldc % 4 || slot_floats % 4) return false;
-  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
-                              static_cast<cuuint64_t>(slots)};
-  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ldc) * 4, static_cast<cuuint64_t>(W) * ldc * 4,
-                                 static_cast<cuuint64_t>(slot_floats) * 4};
-  const cuuint32_t box[4] = {static_cast<cuuint32_t>(g.g), static_cast<cuuint32_t>(g.Wb * stride),
-                             static_cast<cuuint32_t>(g.Hb * stride), 1};
-  const cuuint32_t elem[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, elem,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, g.g == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-bool conv_window_geometry(int Cin, int KH, int KW, int Ho, int Wo, int stride, WinGeom* wg) {
-  if (KH * KW <= 1) return false;
-  WinGeom w;
-  if (!conv_act_geometry(Cin, Ho, Wo, stride, &w.act)) return false;
-  const int g = Cin % 32 == 0 ? 32 : (Cin == 4 || Cin == 8 || Cin == 16) ? Cin : 0;
-  if (!g) return false;
-  w.act.g = g;
-  w.Win = (Wo - 1) * stride + KW;
-  w.Hin = (w.act.Hb - 1) * stride + KH;
-  if (w.Win > 256 || w.Hin > 256) return false;
-  w.ktpc = (KH * KW * g + conv_tc::kBK - 1) / conv_tc::kBK;
-  w.Kwin = (Cin / g) * w.ktpc * conv_tc::kBK;
-  w.tx_bytes = w.Win * w.Hin * g * 4;
-  w.img_bytes = (w.tx_bytes + 1023) / 1024 * 1024;
-  if (w.act.G * w.img_bytes > conv_tc::kWinBytes) return false;
-  *wg = w;
-  return true;
-}
-
-void conv_window_weights(const float* w, int N, int Kpad_src, int KH, int KW, int Cin, const WinGeom& wg,
-                         float* out) {
-  const int g = wg.act.g, taps = KH * KW, tpk_total = wg.ktpc * conv_tc::kBK / g;
-  for (int n = 0; n < N; ++n) {
-    float* o = out + static_cast<std::size_t>(n) * wg.Kwin;
-    const float* src = w + static_cast<std::size_t>(n) * Kpad_src;
-    for (int c = 0; c < Cin / g; ++c)
-      for (int t = 0; t < tpk_total; ++t)
-        for (int ci = 0; ci < g; ++ci)
-          o[(c * tpk_total + t) * g + ci] = t < taps ? src[t * Cin + c * g + ci] : 0.f;
-  }
-}
-
 bool conv_tap_rows_eligible(int Cin, int KW) {
   if (Cin != 4 && Cin != 8 && Cin != 16) return false;
   const int taps = conv_tc::kBK / Cin;
@@ -203,50 +134,6 @@ void conv_tap_row_weights(const float* w, int N, int Kpad_src, int KH, int KW, i
         for (int ci = 0; ci < Cin; ++ci)
           o[(kh * taps + kw) * Cin + ci] = kw < KW ? src[(kh * KW + kw) * Cin + ci] : 0.f;
   }
-}
-
-bool encode_window_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
-                       long slot_floats, const WinGeom& wg) {
-  const EncodeTiledFn encode = encode_fn();
-  if (!encode || (reinterpret_cast<uintptr_t>(base) & 15) || ldc % 4 || slot_floats % 4) return false;
-  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
-                              static_cast<cuuint64_t>(slots)};
-  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ldc) * 4, static_cast<cuuint64_t>(W) * ldc * 4,
-                                 static_cast<cuuint64_t>(slot_floats) * 4};
-  const cuuint32_t box[4] = {static_cast<cuuint32_t>(wg.act.g), static_cast<cuuint32_t>(wg.Win),
-                             static_cast<cuuint32_t>(wg.Hin), 1};
-  const cuuint32_t elem[4] = {1, 1, 1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, elem,
-                CU_TENSOR_MAP_INTERLEAVE_NONE,
-                wg.act.g == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-void conv_use_window(ConvParams& p, const CUtensorMap& amap, const CUtensorMap& wmap, const WinGeom& wg,
-                     const float* slot_base, long slot_floats, long slots) {
-  conv_use_act_map(p, amap, wg.act, slot_base, slot_floats, slots);
-  p.wmap = wmap;
-  p.a_win = 1;
-  p.Win = wg.Win;
-  p.Hin = wg.Hin;
-  p.ktpc = wg.ktpc;
-  p.win_img_bytes = wg.img_bytes;
-  p.win_tx_bytes = wg.tx_bytes;
-  p.Kpad = wg.Kwin;
-}
-
-void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& g, const float* slot_base,
-                      long slot_floats, long slots) {
-  p.amap = map;
-  p.a_tma = 1;
-  p.a_g = g.g;
-  p.Wb = g.Wb;
-  p.Hb = g.Hb;
-  p.G = g.G;
-  p.tpi = g.tpi;
-  p.slot_base = slot_base;
-  p.slot_floats = slot_floats;
-  p.oob_slot = static_cast<int>(slots);
 }
 
 namespace {
@@ -307,18 +194,12 @@ cudaError_t launch_conv_tc(ConvParams p, cudaStream_t stream) {
   int bn = conv_tile_n(p.N);
   const int sms = sm_count();
   const int KT = p.Kpad / conv_tc::kBK;
-  if (p.a_tma && (p.G < 1 || p.G > 4 || p.Wb * p.Hb * p.G != conv_tc::kBM || p.a_g % 4 || p.Cin % p.a_g))
+  if (p.tap_rows && (!conv_tap_rows_eligible(p.Cin, p.KW) || p.Kpad != p.KH * conv_tc::kBK))
     return cudaErrorInvalidValue;
-  if (p.tap_rows && (p.a_tma || !conv_tap_rows_eligible(p.Cin, p.KW) || p.Kpad != p.KH * conv_tc::kBK))
-    return cudaErrorInvalidValue;
-  if (p.a_win && (!p.a_tma || bn > 128 || p.G * p.win_img_bytes > conv_tc::kWinBytes || p.ktpc <= 0 ||
-                  p.Kpad != (p.Cin / p.a_g) * p.ktpc * conv_tc::kBK))
-    return cudaErrorInvalidValue;
-  p.m_tiles = p.a_tma ? (p.G == 1 ? p.nimg * p.tpi : (p.nimg + p.G - 1) / p.G)
-                      : (p.nimg * p.Ho * p.Wo + conv_tc::kBM - 1) / conv_tc::kBM;
+  p.m_tiles = (p.nimg * p.Ho * p.Wo + conv_tc::kBM - 1) / conv_tc::kBM;
   if (use_wide(p, sms)) {
     bn = 256;
-    p.wmap = p.wmap_wide;
+    p.wmap = *p.wmap_wide;
   }
   p.n_tiles = (p.N + bn - 1) / bn;
   const int tiles = p.m_tiles * p.n_tiles;
@@ -327,8 +208,6 @@ cudaError_t launch_conv_tc(ConvParams p, cudaStream_t stream) {
   // overhead); a split launch has one CTA per unit (cluster = the splits).
   int ks = choose_ksplits(tiles, KT, sms);
   if (p.ks_force > 0) ks = std::min({p.ks_force, 8, KT});  // measured choice (executor autotune)
-  static const int dbg = std::getenv("BS_CONV_DEBUG") ? std::atoi(std::getenv("BS_CONV_DEBUG")) : 0;
-  p.debug = dbg;
   // n-minor unit order (opt-in BS_CONV_NMINOR=1): an M tile's activations
   // are re-read for each N tile while still in L2 (1x1 56x56 64->256 +
   // residual at b=90: 190 -> 184 us; ResNet-50 layer sum -1%), but the e2e
@@ -341,16 +220,16 @@ cudaError_t launch_conv_tc(ConvParams p, cudaStream_t stream) {
   const int grid = p.ksplits > 1 ? units : std::min(units, sms);
   static const bool log = std::getenv("BS_CONV_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d tma=%d win=%d box=%dx%dx%d g=%d\n",
-                 p.nimg * p.Ho * p.Wo, p.N, p.K, KT, bn, tiles, p.ksplits, grid, p.a_tma, p.a_win, p.Hb, p.Wb, p.G, p.a_g);
+    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d tiles=%d ks=%d grid=%d tap_rows=%d\n",
+                 p.nimg * p.Ho * p.Wo, p.N, p.K, KT, bn, tiles, p.ksplits, grid, p.tap_rows);
   p.group_units = 0;
   return launch_dispatch(p, p, bn, grid, stream);
 }
 
 cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream, bool force, int ks) {
   for (const ConvParams* q : {&a, &b})
-    if (q->Cin % 4 != 0 || q->Kpad % conv_tc::kBK != 0 || q->Kpad < q->K || q->nimg <= 0 || q->a_tma ||
-        q->a_win || q->tap_rows || q->prec != a.prec)
+    if (q->Cin % 4 != 0 || q->Kpad % conv_tc::kBK != 0 || q->Kpad < q->K || q->nimg <= 0 || q->tap_rows ||
+        q->prec != a.prec)
       return cudaErrorInvalidValue;
   const int bn = std::max(conv_tile_n(a.N), conv_tile_n(b.N));
   // Unforced, a group is unsplit: decline (the caller launches the two convs
@@ -364,13 +243,11 @@ cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream
     t.m_tiles = (q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM;
     if (use_wide(t, sm_count())) return cudaErrorNotSupported;  // 128 x 256 tiles beat the group
   }
-  static const int dbg = std::getenv("BS_CONV_DEBUG") ? std::atoi(std::getenv("BS_CONV_DEBUG")) : 0;
   ks = force ? std::max(1, std::min({ks, 8, a.Kpad / conv_tc::kBK, b.Kpad / conv_tc::kBK})) : 1;
   for (ConvParams* q : {&a, &b}) {
     q->m_tiles = (q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM;
     q->n_tiles = (q->N + bn - 1) / bn;
     q->ksplits = ks;
-    q->debug = dbg;
     q->group_units = 0;
     const char* nm = std::getenv("BS_CONV_NMINOR");
     q->n_minor = nm ? (nm[0] == '1') : 0;
@@ -381,7 +258,7 @@ cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream
   const int grid = ks > 1 ? units : std::min(units, sm_count());
   static const bool log = std::getenv("BS_CONV_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d units=%d ks=%d grid=%d tma=0 win=0 group=M%dN%dK%d\n",
+    std::fprintf(stderr, "conv M=%d N=%d K=%d KT=%d bn=%d units=%d ks=%d grid=%d group=M%dN%dK%d\n",
                  a.nimg * a.Ho * a.Wo, a.N, a.K, a.Kpad / conv_tc::kBK, bn, units, ks, grid, b.nimg * b.Ho * b.Wo,
                  b.N, b.K);
   return launch_dispatch(a, b, bn, grid, stream);

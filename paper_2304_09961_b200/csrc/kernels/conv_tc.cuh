@@ -33,10 +33,9 @@
 //     two MMAs per K step and no extra HBM or shared-memory traffic (A_lo
 //     lives in TMEM next to A_hi).
 //
-// Warp roles: 0-3 A cp.async producers (or, with TMA activations, the second
-// converter group), 4-7 epilogue (TMEM lanes 0-127), 8 MMA issuer (+ TMEM
-// owner), 9 B TMA issuer, 10-13 A converters (group 0), 14 A TMA issuer,
-// 15-18 A converters (group 1, cp.async gather).
+// Warp roles: 0-3 A cp.async producers, 4-7 epilogue (TMEM lanes 0-127),
+// 8 MMA issuer (+ TMEM owner), 9 B TMA issuer, 10-13 A converters (group 0),
+// 14 idle, 15-18 A converters (group 1).
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -74,26 +73,6 @@ struct ConvParams {
   // work decomposition (filled by launch_conv_tc)
   int m_tiles, n_tiles, ksplits;  // K tiles of split s: [s KT / ksplits, (s + 1) KT / ksplits)
   unsigned long long* trace;    // debug timeline of CTA 0 (nullptr in production)
-  // TMA activation path (a_tma = 1): A tiles are (Hb x Wb) output-pixel boxes
-  // of one image each, loaded per filter tap by a 4D tensor map over the whole
-  // slot space {C, W, H, slot} (zero fill = padding, element strides = conv
-  // stride). G = 128 / (Hb * Wb) images per 128-row M tile.
-  CUtensorMap amap;
-  int a_tma;
-  int a_g;                      // channels per box (32, 16, 8 or 4)
-  int Wb, Hb, G, tpi;           // box geometry; tpi = M tiles per image (G == 1)
-  const float* slot_base;       // slot index of an image = (in_ptrs[i] - slot_base) / slot_floats
-  long slot_floats;
-  int oob_slot;                 // a slot coordinate past the map (zero-filled boxes)
-  // Window mode (a_win = 1, spatial convs; implies a_tma): per M tile and
-  // channel chunk of g, one TMA box brings the input window Hin x Win x g of
-  // each image; converter warps expand the im2col rows of all taps from it.
-  // K order is chunk-major ((chunk, tap, ci), ktpc K tiles per chunk, padded
-  // taps zero) and the weights (wmap) are laid out to match.
-  int a_win;
-  int Win, Hin, ktpc;
-  int win_img_bytes;            // smem stride between the G image windows (1024-aligned)
-  int win_tx_bytes;             // bytes one image window box delivers
   // Tap-row mode (Cin * 32 / Cin taps = one K tile per filter row): K order
   // (kh, kw < 32 / Cin, ci) with zero weights past KW, Kpad = KH * 32. Each
   // output pixel's A row of a K tile is 32 / Cin consecutive input pixels
@@ -111,9 +90,9 @@ struct ConvParams {
   // the split count (clamped to the K tiles and the cluster limit of 8).
   int ks_force;
   int n_minor;                  // unit order (see unit_of)
-  int debug;                    // experiment switches (0 in production; BS_CONV_DEBUG)
-  CUtensorMap wmap_wide;        // weights with a 256-row box (N > 128), used for 128 x 256 tiles
-  int has_wide;
+  // Host side only (the launcher swaps it into wmap for 128 x 256 tiles):
+  // weights map with a 256-row box (N > 128), owned by the caller.
+  const CUtensorMap* wmap_wide;
 };
 
 
@@ -121,7 +100,6 @@ namespace conv_tc {
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // fp32 elements per 128-byte K row
-constexpr int kWinBytes = 65536;  // one input window (window mode); two share the raw A ring
 
 // Pipeline geometry per N tile. Three rings decouple the stages so no load
 // waits on an MMA it does not feed:
@@ -162,7 +140,6 @@ struct Cfg {
   static constexpr int kTotal = kBarOffset + 512 + 1024;        // barriers + alignment slack
   static_assert(kTotal <= 232448, "shared memory budget");
   static_assert(TA >= 2, "TMEM budget");
-  static_assert(BN == 256 || RA * kABytes >= 2 * kWinBytes, "window ring");
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -201,28 +178,13 @@ __device__ __forceinline__ Unit unit_of(const ConvParams& p, int u, int BN, int 
 }
 
 // Output pixel of row r of M tile mt: image and pixel index, false for
-// padding rows (M tail; box columns/rows outside the output in TMA mode).
+// padding rows (M tail).
 __device__ __forceinline__ bool row_pixel(const ConvParams& p, int mt, int r, int& img, int& pix) {
-  if (!p.a_tma) {
-    const int m = mt * kBM + r;
-    const int HoWo = p.Ho * p.Wo;
-    img = m / HoWo;
-    pix = m - img * HoWo;
-    return m < p.nimg * HoWo;
-  }
-  const int R = kBM / p.G;
-  const int b = r / R, rr = r - b * R;
-  const int dh = rr / p.Wb, dw = rr - dh * p.Wb;
-  int h;
-  if (p.G == 1) {
-    img = mt / p.tpi;
-    h = (mt - img * p.tpi) * p.Hb + dh;
-  } else {
-    img = mt * p.G + b;
-    h = dh;
-  }
-  pix = h * p.Wo + dw;
-  return img < p.nimg && h < p.Ho && dw < p.Wo;
+  const int m = mt * kBM + r;
+  const int HoWo = p.Ho * p.Wo;
+  img = m / HoWo;
+  pix = m - img * HoWo;
+  return m < p.nimg * HoWo;
 }
 
 // A operand conversion. 2xTF32: hi = x with the 13 low mantissa bits
@@ -276,11 +238,30 @@ __device__ __forceinline__ float epilogue_op(const ConvParams& p, float x, int n
   return x;
 }
 
+// Kernel parameters: one problem, or two for a grouped launch (an ungrouped
+// launch does not ship a second ConvParams: the parameter block is what the
+// host pays per launch).
+template <bool GROUP>
+struct ConvArgs {
+  ConvParams a;
+};
+template <>
+struct ConvArgs<true> {
+  ConvParams a, b;
+};
+template <bool GROUP>
+__device__ __forceinline__ const ConvParams& second_problem(const ConvArgs<GROUP>& k) {
+  if constexpr (GROUP) return k.b;
+  else return k.a;
+}
+
 template <int BN, int PREC, bool GROUP>
 __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
-    conv_tc_kernel(const __grid_constant__ ConvParams p_a, const __grid_constant__ ConvParams p_b) {
+    conv_tc_kernel(const __grid_constant__ ConvArgs<GROUP> args) {
   // Roles take the problem of each unit from BS_UNIT_PROBLEM (p_a for the
   // first units0 units, p_b after); outside unit loops p is p_a.
+  const ConvParams& p_a = args.a;
+  const ConvParams& p_b = second_problem<GROUP>(args);
   const ConvParams& p = p_a;
   using S = Cfg<BN, PREC>;
   constexpr bool SPLIT = PREC == 1, BF16 = PREC == 2;
@@ -297,9 +278,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
   uint64_t* b_empty = ta_empty;        // same ring: one commit frees slot and stage
   uint64_t* acc_full = ta_empty + TA;  // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
-  uint64_t* win_full = acc_empty + 2;  // [2] window mode
-  uint64_t* win_empty = win_full + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(win_empty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -322,8 +301,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RA; ++s) {
-      // TMA: one arrive.expect_tx; cp.async: one .noinc arrival per producer thread
-      ptx::mbar_init(&ra_full[s], p.a_tma ? 1 : 128);
+      // one cp.async .noinc arrival per producer thread
+      ptx::mbar_init(&ra_full[s], 128);
       ptx::mbar_init(&ra_empty[s], 128);
     }
     for (int s = 0; s < NB; ++s) {
@@ -336,8 +315,6 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
       ptx::mbar_init(&acc_empty[a], 128);
-      ptx::mbar_init(&win_full[a], 1);
-      ptx::mbar_init(&win_empty[a], 256);  // both converter groups, once per window
     }
     ptx::fence_mbar_init();
   }
@@ -345,7 +322,6 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
     ptx::prefetch_tmap(&p_a.wmap);
     if (GROUP) ptx::prefetch_tmap(&p_b.wmap);
   }
-  if (warp == 0 && lane == 0 && p.a_tma) ptx::prefetch_tmap(&p.amap);
   if (warp == 8) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
@@ -360,114 +336,9 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
 
   // Converter: thread = one A row (TMEM lane). Reads its 128-byte row of a
   // landed raw stage, frees the stage, and writes the MMA operand into its
-  // TMEM lane: rn_tf32(a) (+ the residual a - rn_tf32(a) for 2xTF32). With
-  // TMA activations two converter groups (warps 10-13 and 0-3) take
-  // alternate K tiles so the conversion latency overlaps.
-  // Images of an M tile (TMA geometry): slot index and first output row.
-  auto tile_slots = [&](const Unit& w, int (&slot)[4], int (&h0)[4]) {
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      int img;
-      if (p.G == 1) {
-        img = w.mt / p.tpi;
-        h0[b] = (w.mt - img * p.tpi) * p.Hb;
-      } else {
-        img = w.mt * p.G + b;
-        h0[b] = 0;
-      }
-      slot[b] = (b < p.G && img < p.nimg) ? static_cast<int>((p.in_ptrs[img] - p.slot_base) / p.slot_floats)
-                                          : p.oob_slot;
-    }
-  };
-
-  // Window-mode converter: the same TMEM hand-off as convert(), but the 32
-  // K values of a row are read from the chunk's input window (taps of one
-  // channel chunk), so each input element enters the SM once per M tile.
-  auto convert_window = [&](int group, int ngroups, int trace_tid) {
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const int R = kBM / p.G;
-    const int b = row / R, rr = row - b * R;
-    const int dh = rr / p.Wb;
-    const int dw = min(rr - dh * p.Wb, p.Wo - 1);  // padding columns re-read a valid pixel
-    const int pix0 = dh * p.stride * p.Win + dw * p.stride;
-    const uint32_t win0 = smem_base + static_cast<uint32_t>(b * p.win_img_bytes);
-    const int g = p.a_g, tpk = kBK / g, taps = p.KH * p.KW;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + S::kTA0;
-    int it = 0, wi = -1;
-    bool waited = false;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const Unit w = unit_of(p, u, BN, KT);
-      for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-        const int c = kt / p.ktpc, jt = kt - c * p.ktpc;
-        if (kt == w.kt0 || jt == 0) {
-          ++wi;
-          waited = false;
-        }
-        const uint32_t win = win0 + static_cast<uint32_t>((wi & 1) * kWinBytes);
-        if (it % ngroups == group) {
-          if (!waited) {
-            ptx::mbar_wait(&win_full[wi & 1], (wi >> 1) & 1);
-            waited = true;
-          }
-          if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 2] = gtime();
-          float4 v[8];
-          if (g == kBK) {
-            const int t = jt;
-            if (t < taps) {
-              const int kh = t / p.KW, kw = t - kh * p.KW;
-              const int pix = pix0 + kh * p.Win + kw;
-#pragma unroll
-              for (int cc = 0; cc < 8; ++cc) v[cc] = ptx::lds128(win + swz(pix, cc));
-            } else {
-#pragma unroll
-              for (int cc = 0; cc < 8; ++cc) v[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-          } else {
-            const int cpt = g / 4;  // 16-byte chunks per tap
-#pragma unroll
-            for (int cc = 0; cc < 8; ++cc) {
-              const int j = cc / cpt, c4 = cc - j * cpt;
-              const int t = jt * tpk + j;
-              if (t < taps) {
-                const int kh = t / p.KW, kw = t - kh * p.KW;
-                v[cc] = ptx::lds128(win + (pix0 + kh * p.Win + kw) * (g * 4) + c4 * 16);
-              } else {
-                v[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
-              }
-            }
-          }
-          uint32_t hi[32];
-          [[maybe_unused]] uint32_t lo[32];
-          a_operand<PREC>(v, hi, lo);
-          const int sa = it % TA;
-          const bool tr = p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48;
-          if (tr) p.trace[2048 + it * 4 + 0] = gtime();
-          if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
-          if (tr) p.trace[2048 + it * 4 + 1] = gtime();
-          ptx::tc_fence_after();
-          const uint32_t dst = lane_base + sa * S::kACols;
-          a_store<PREC>(dst, hi, lo);
-          if (tr) p.trace[2048 + it * 4 + 2] = gtime();
-          ptx::tmem_st_wait();
-          if (tr) p.trace[2048 + it * 4 + 3] = gtime();
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&ta_full[sa]);
-          if (tr) p.trace[1024 + it * 5 + 3] = gtime();
-        }
-        if (jt == p.ktpc - 1 || kt == w.kt1 - 1) {
-          // Done with this window (own reads complete); waiting for its fill
-          // first keeps the arrival in the window's own release phase.
-          if (!waited) {
-            ptx::mbar_wait(&win_full[wi & 1], (wi >> 1) & 1);
-            waited = true;
-          }
-          ptx::mbar_arrive(&win_empty[wi & 1]);
-        }
-      }
-    }
-  };
-
+  // TMEM lane (TF32 hi (+ lo for 2xTF32), or packed bf16 pairs). Two
+  // converter groups (warps 10-13 and 15-18) take alternate K tiles so the
+  // conversion latency overlaps.
   auto convert = [&](int group, int ngroups, int trace_tid) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
@@ -486,21 +357,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
         if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 2] = gtime();
         const uint32_t a_raw = smem_base + s * S::kABytes;
         float4 v[8];
-        if (p.debug & 16) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) v[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        } else if (!p.a_tma || p.a_g == kBK) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) v[c] = ptx::lds128(a_raw + roff[c]);
-        } else {
-          // TMA pieces of g channels: piece j = [128 rows][g] floats.
-          const int cpp = p.a_g / 4;  // 16-byte chunks per row of a piece
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int j = c / cpp, cc = c - j * cpp;
-            v[c] = ptx::lds128(a_raw + j * (kBM * p.a_g * 4) + row * (p.a_g * 4) + cc * 16);
-          }
-        }
+        for (int c = 0; c < 8; ++c) v[c] = ptx::lds128(a_raw + roff[c]);
         ptx::mbar_arrive(&ra_empty[s]);
         uint32_t hi[32];
         [[maybe_unused]] uint32_t lo[32];
@@ -509,10 +367,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
         if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t dst = lane_base + sa * S::kACols;
-        if (!(p.debug & 1)) {
-          a_store<PREC>(dst, hi, lo);
-          ptx::tmem_st_wait();
-        }
+        a_store<PREC>(dst, hi, lo);
+        ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&ta_full[sa]);
         if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 3] = gtime();
@@ -520,70 +376,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
     }
   };
 
-  if (warp < 4 && p.a_win) {
-    convert_window(1, 2, 0);
-  } else if (warp < 4 && p.a_tma) {
-    convert(1, 2, 0);
-  } else if (warp == 14) {
-    if (p.a_win && lane == 0) {
-      // ------------------------------------------ input windows by TMA
-      int wi = -1, it = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit w = unit_of(p, u, BN, KT);
-        int slot[4], h0[4];
-        tile_slots(w, slot, h0);
-        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-          const int c = kt / p.ktpc, jt = kt - c * p.ktpc;
-          if (kt != w.kt0 && jt != 0) continue;
-          if (p.trace && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
-          ++wi;
-          if (wi >= 2) ptx::mbar_wait(&win_empty[wi & 1], ((wi >> 1) - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&win_full[wi & 1], static_cast<uint32_t>(p.G * p.win_tx_bytes));
-          const uint32_t win = smem_base + static_cast<uint32_t>((wi & 1) * kWinBytes);
-          for (int b = 0; b < p.G; ++b)
-            ptx::tma_load_4d(win + b * p.win_img_bytes, &p.amap, c * p.a_g, -p.pad, h0[b] * p.stride - p.pad,
-                             slot[b], &win_full[wi & 1]);
-        }
-      }
-    }
-    // ------------------------------------------------------ A by TMA boxes
-    // K tile kt = 32 / g boxes per image of the tile: k = kt * 32 + j * g
-    // -> (tap, ci); box origin = (ci, w0 * s - pad + kw, h0 * s - pad + kh,
-    // slot). Boxes past K or past the batch are aimed outside the map so the
-    // stage is zero-filled and the byte count stays constant.
-    else if (p.a_tma && lane == 0) {
-      const int R = kBM / p.G;
-      const int pieces = kBK / p.a_g;
-      const uint32_t box_bytes = static_cast<uint32_t>(R * p.a_g * 4);
-      int it = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit w = unit_of(p, u, BN, KT);
-        int slot[4], h0[4];
-        tile_slots(w, slot, h0);
-        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-          const int s = it % RA;
-          if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&ra_full[s], S::kABytes);
-          const uint32_t a_tile = smem_base + s * S::kABytes;
-          for (int j = 0; j < pieces; ++j) {
-            const int k = kt * kBK + j * p.a_g;
-            int tap = k / p.Cin;
-            int ci = k - tap * p.Cin;
-            if (k >= p.K) {
-              tap = 0;
-              ci = p.Cin;  // past dim 0: zeros
-            }
-            const int kh = tap / p.KW, kw = tap - kh * p.KW;
-            for (int b = 0; b < p.G; ++b)
-              ptx::tma_load_4d(a_tile + j * (kBM * p.a_g * 4) + b * box_bytes, &p.amap, ci, kw - p.pad,
-                               h0[b] * p.stride - p.pad + kh, slot[b], &ra_full[s]);
-          }
-          if (p.trace && it == 0) p.trace[8 + 4 * blockIdx.x + 2] = gtime();
-          if (p.trace && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 0] = gtime();
-        }
-      }
-    }
-  } else if (warp < 4) {
+  if (warp < 4) {
+    // ------------------------------------------------------------ A gather  } else if (warp < 4) {
     // ------------------------------------------------------------ A gather
     const int t = threadIdx.x;
     const int c = t & 7;    // 16-byte chunk inside the 128-byte K row
@@ -866,13 +660,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
       if (p.ksplits == 1) {
         const bool ok = (reinterpret_cast<uintptr_t>(out_row) & 15) == 0 &&
                         (reinterpret_cast<uintptr_t>(res_row) & 15) == 0 && (!p.res_ptrs || !out_row || res_row);
-        fast = __all_sync(0xffffffffu, ok) && (p.N & 3) == 0 && !(p.debug & 4) && !(p.res_ptrs && (p.debug & 8));
+        fast = __all_sync(0xffffffffu, ok) && (p.N & 3) == 0;
       }
       // Residual rows: this lane's row segment of a 32-column chunk into L1
       // one chunk ahead (the quads are read right after the TMEM load).
       auto prefetch_res = [&](int c) {
         const int n0 = w.n_base + c * 32;
-        if (res_row && n0 < p.N && !(p.debug & 64)) {
+        if (res_row && n0 < p.N) {
           ptx::prefetch_l1(res_row + n0);
           ptx::prefetch_l1(res_row + min(n0 + 31, p.N - 1));
         }
@@ -883,11 +677,6 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
       ptx::mbar_wait(&acc_full[acc], (j / S::kAcc) & 1);
       if (etr) p.trace[3072 + j * 8 + 1] = gtime();
       ptx::tc_fence_after();
-      if (p.debug & 32) {  // timing experiment: release the accumulator untouched
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&acc_empty[acc]);
-        continue;
-      }
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       if (p.ksplits == 1) {
         // Coalesced epilogue: each warp stages its 32 rows x 32 columns in
@@ -974,7 +763,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
             const int rl = rq * 4 + (lane >> 3);  // row inside the warp's 32
             const unsigned long long op = fin_out[rl];
             const unsigned long long rp = fin_res[rl];
-            if (!op || !col_ok || (p.debug & 4)) return;
+            if (!op || !col_ok) return;
             float4 x = ptx::lds128(stage + rl * 128 + ((cq ^ (rl & 7)) << 4));
             float* dst = reinterpret_cast<float*>(op) + nc;
             const float* rr = reinterpret_cast<const float*>(rp);
@@ -1080,7 +869,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
               // A: 8 TMEM columns per K=8 step; B: +32 bytes inside the swizzled row.
               ptx::mma_tf32_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
               if constexpr (SPLIT)
-                if (!(p.debug & 2)) ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
+                ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
             }
           }
           ptx::mma_commit(&ta_empty[sa]);  // == b_empty[sb]
@@ -1107,9 +896,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
     }
     __syncwarp();
   } else if (warp >= 10 && warp < 14) {
-    if (p.a_win) convert_window(0, 2, 320);
-    else convert(0, 2, 320);
-  } else if (warp >= 15 && warp < 19 && !p.a_win && !p.a_tma) {
+    convert(0, 2, 320);
+  } else if (warp >= 15 && warp < 19) {
     convert(1, 2, 480);
   }
 
@@ -1169,52 +957,17 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
 // conv_add_wide_map).
 int conv_tile_n(int N);
 
-// Box geometry of the TMA activation path for a conv with Cin (padded)
-// input channels and an Ho x Wo output: Wb = next power of two >= Wo,
-// Hb = min(128 / Wb, next power of two >= Ho), G = 128 / (Wb * Hb) images per
-// M tile, g = channels per box. False when the layer does not fit the path
-// (tiny outputs such as FC layers, G > 4): it then uses the cp.async gather.
-struct ActGeom {
-  int Wb = 0, Hb = 0, G = 0, tpi = 0, g = 0;
-};
-bool conv_act_geometry(int Cin, int Ho, int Wo, int stride, ActGeom* geom);
-// Tensor map over a slot space of `slots` request blobs of `slot_floats`
-// floats each: {C, W, H, slot} starting at `base` (the tensor's first channel
-// in slot 0), box {g, Wb * stride, Hb * stride, 1}, element strides
-// {1, stride, stride, 1}; 128B swizzle when g == 32.
-bool encode_act_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
-                    long slot_floats, const ActGeom& geom, int stride);
-// Window mode for a KH x KW (> 1) conv: channel chunk g = 32 (or Cin when
-// Cin is 4, 8 or 16), window Hin x Win per image, ktpc K tiles per chunk and
-// the chunk-major K extent Kwin. False when the window does not fit a 64 KB
-// buffer (the conv then uses the gather paths).
-struct WinGeom {
-  ActGeom act;
-  int Win = 0, Hin = 0, ktpc = 0, Kwin = 0, img_bytes = 0, tx_bytes = 0;
-};
-bool conv_window_geometry(int Cin, int KH, int KW, int Ho, int Wo, int stride, WinGeom* wg);
-// Chunk-major copy of a [N][Kpad_src] (tap-major K = (kh, kw, ci)) weight
-// matrix: out[N][Kwin].
-void conv_window_weights(const float* w, int N, int Kpad_src, int KH, int KW, int Cin, const WinGeom& wg,
-                         float* out);
 // Tap-row mode eligibility (Cin 4 / 8 / 16 and at most one padded tap per
 // filter row: the stems) and the matching weight layout out[N][KH * 32].
 bool conv_tap_rows_eligible(int Cin, int KW);
 void conv_tap_row_weights(const float* w, int N, int Kpad_src, int KH, int KW, int Cin, float* out);
-// Window tensor map: {C, W, H, slot} box {g, Win, Hin, 1}.
-bool encode_window_map(CUtensorMap* map, const float* base, int C, int W, int H, int ldc, long slots,
-                       long slot_floats, const WinGeom& wg);
-void conv_use_window(ConvParams& p, const CUtensorMap& amap, const CUtensorMap& wmap, const WinGeom& wg,
-                     const float* slot_base, long slot_floats, long slots);
-// Fills the TMA fields of p (a_tma = 1) from a geometry and an encoded map.
-void conv_use_act_map(ConvParams& p, const CUtensorMap& map, const ActGeom& geom, const float* slot_base,
-                      long slot_floats, long slots);
 // Encodes a weight tensor map for w ([N][Kpad] floats) and the tile conv_tile_n(N).
 bool encode_weight_map(CUtensorMap* map, const float* w, int N, int Kpad, int box_n = 0);
 // The same for a bf16 copy of the weights (BF16 precision): box {32, BN},
 // 64-byte swizzle.
 bool encode_weight_map_bf16(CUtensorMap* map, const void* w_bf16, int N, int Kpad, int box_n = 0);
-// Offers the launcher 128 x 256 tiles (weights map with box_n = 256).
+// Offers the launcher 128 x 256 tiles (weights map with box_n = 256; the map
+// must outlive the launch call).
 void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide);
 // Grouped launch of two independent convs (no data flow between them; same
 // precision; cp.async gather path, no split-K): one persistent grid walks the

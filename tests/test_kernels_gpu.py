@@ -78,8 +78,7 @@ CASES = [
     dict(nimg=2, H=9, W=9, Cin=24, N=16, KH=1, KW=1, stride=1, pad=0),
     dict(nimg=3, H=1, W=1, Cin=128, N=10, KH=1, KW=1, stride=1, pad=0),
     dict(nimg=2, H=14, W=14, Cin=64, N=48, KH=1, KW=1, stride=2, pad=0),
-    # TMA activation boxes: two images per M tile (odd batch), 16/8-channel
-    # boxes crossing filter taps, stride-2 boxes.
+    # small channel counts, odd batches, stride 2
     dict(nimg=3, H=7, W=7, Cin=16, N=32, KH=3, KW=3, stride=1, pad=1),
     dict(nimg=2, H=14, W=14, Cin=48, N=64, KH=3, KW=3, stride=1, pad=1),
     dict(nimg=2, H=56, W=56, Cin=24, N=144, KH=1, KW=1, stride=1, pad=0),
@@ -192,14 +191,6 @@ def test_maxpool_stride1_tiles(block, H, ceil, monkeypatch):
     (BS_POOL_BLOCK), partial tiles at the right / bottom edges."""
     monkeypatch.setenv("BS_POOL_BLOCK", block)
     test_maxpool_in_executor_layers(3, 1, 1, ceil, H)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("case", CASES[:4] + CASES[10:], ids=lambda c: "x".join(str(c[k]) for k in ("nimg", "H", "Cin", "N", "KH", "stride")))
-def test_conv_tma_activation_path(case, monkeypatch):
-    """TMA activation boxes (BS_CONV_TMA=1) on the same layers as the cp.async gather."""
-    monkeypatch.setenv("BS_CONV_TMA", "1")
-    assert run_conv(**case) < TOL
 
 
 @pytest.mark.gpu

@@ -13,6 +13,8 @@ import bench  # noqa: E402
 from paper_2304_09961_b200.executor import Executor  # noqa: E402
 
 cfgn = int(sys.argv[1])
+DEPTH = int(os.environ.get("DEPTH", "2"))
+D_OVERRIDE = float(os.environ["DEADLINE_MS"]) if os.environ.get("DEADLINE_MS") else None
 rates = [float(x) for x in sys.argv[2:]] or [1000, 2000, 4000]
 cfg = bench.CONFIGS[cfgn]
 mb = cfg["max_batch"]
@@ -30,7 +32,7 @@ def dnn_ms(d, b):
 for d in prof["dnns"]:
     print(d["id"], "T1 %.3f ms  T%d %.3f ms" % (dnn_ms(d, 1), mb, dnn_ms(d, mb)))
 t1 = max(dnn_ms(d, 1) for d in prof["dnns"])
-deadline = round(6.25 * t1, 3)
+deadline = D_OVERRIDE or round(6.25 * t1, 3)
 sim = {"scheduler": cfg["scheduler"], "granularity": cfg["granularity"], "max_batch": mb}
 if "shared_batching" in cfg:
     sim["shared_batching"] = cfg["shared_batching"]
@@ -39,7 +41,7 @@ for proc in ([cfg["process"], "poisson"] if cfg["process"] != "poisson" else ["p
         w = {"process": proc, "rate": rate, "count": 3000, "seed": 11, "relative_deadline": deadline}
         if len(names) > 1:
             w["dnn_mix"] = [[n, 1.0 / len(names)] for n in names]
-        job = {"profile": prof, "sim": sim, "image_pool": 64, "pipeline_depth": 2, "workload": w}
+        job = {"profile": prof, "sim": sim, "image_pool": 64, "pipeline_depth": DEPTH, "workload": w}
         ex.stats(True, every=1)
         r = ex.serve(job)
         s = ex.stats_summary(6550.0, 696.0)
