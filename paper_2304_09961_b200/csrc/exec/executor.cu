@@ -945,6 +945,38 @@ double Executor::profile_layer(int dnn, int layer, int batch, int reps, bool flu
   return ms[ms.size() / 2];
 }
 
+std::vector<double> Executor::profile_pass(int dnn, int batch, int reps) {
+  if (batch < 1 || batch > max_batch_) throw std::invalid_argument("profile batch out of range");
+  const int L = suite_.nets[static_cast<std::size_t>(dnn)].num_layers();
+  std::vector<cudaEvent_t> ev(static_cast<std::size_t>(reps) * (L + 1));
+  for (auto& e : ev) ck(cudaEventCreate(&e), "ev");
+  for (int w = 0; w < 2; ++w)
+    for (int k = 1; k <= L; ++k) run_layer(dnn, k, scratch_ptrs_, batch);
+  for (int r = 0; r < reps; ++r) {
+    cudaEvent_t* er = ev.data() + static_cast<std::size_t>(r) * (L + 1);
+    ck(cudaEventRecord(er[0], stream_), "ev");
+    for (int k = 1; k <= L; ++k) {
+      run_layer(dnn, k, scratch_ptrs_, batch);
+      ck(cudaEventRecord(er[k], stream_), "ev");
+    }
+  }
+  ck(cudaStreamSynchronize(stream_), "pass sync");
+  std::vector<double> out(static_cast<std::size_t>(L));
+  std::vector<double> v(static_cast<std::size_t>(reps));
+  for (int k = 1; k <= L; ++k) {
+    for (int r = 0; r < reps; ++r) {
+      float t = 0;
+      const cudaEvent_t* er = ev.data() + static_cast<std::size_t>(r) * (L + 1);
+      ck(cudaEventElapsedTime(&t, er[k - 1], er[k]), "elapsed");
+      v[static_cast<std::size_t>(r)] = t;
+    }
+    std::sort(v.begin(), v.end());
+    out[static_cast<std::size_t>(k - 1)] = v[v.size() / 2];
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return out;
+}
+
 void Executor::profile_span(int dnn, int from, int to, int batch, int reps, double out[3]) {
   if (batch < 1 || batch > max_batch_) throw std::invalid_argument("profile batch out of range");
   cudaEvent_t a, b;

@@ -84,6 +84,11 @@ class Executor {
   // Median of `reps` CUDA-event timings of one layer at batch b (cold L2 if
   // flush), on scratch blobs.
   double profile_layer(int dnn, int layer, int batch, int reps, bool flush_l2);
+  // Per-layer latency inside back-to-back whole-network passes (ms, median
+  // over reps): events between the layers of a pass, the stream kept full
+  // -- the cost a layer has in a multi-layer serving step, without the
+  // launch latency and idle gaps a synchronised single-layer timing adds.
+  std::vector<double> profile_pass(int dnn, int batch, int reps);
   // Layers [from, to] at one batch on scratch blobs, per pass (ms):
   // out[0] = synchronised per pass (launch latency included), out[1] = reps
   // passes queued back to back, out[2] = one CUDA graph of the pass replayed.

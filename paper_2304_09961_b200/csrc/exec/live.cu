@@ -28,6 +28,7 @@ struct Book {
   int dnn = 0;
   double arrival = 0, deadline = 0, completion = -1;
   bool dropped = false, done = false;
+  batchsim::CompletionLocation location = batchsim::CompletionLocation::server;
 };
 
 struct InFlight {
@@ -90,6 +91,51 @@ json serve_live(Executor& ex, const json& j) {
   // ids follow arrival order (the pending queue's binary search relies on it)
   for (std::size_t i = 1; i < n; ++i)
     if (arrivals[i].time < arrivals[i - 1].time) throw std::logic_error("serve: arrivals out of time order");
+
+  // Server admissions: (time at the server, id, entry layer). Without
+  // offload every request arrives at layer 1 at its generation time. In
+  // collaborative mode (config 5) the client side -- per-client compute
+  // queues, the uplink trace, the EWMA throughput estimate and the
+  // binary / partial offload decision (reference simulator.hpp:286-433,
+  // offload.hpp:22-161) -- does not depend on the server, so it is replayed
+  // in virtual time by the reference-semantics Simulator with a recording
+  // hook, and its server arrivals (request id, entry layer) are served live:
+  // the intermediate activation of the client's prefix is computed on the
+  // executor's side stream at admission (Executor::admit, entry_layer > 1).
+  // Requests the client finishes on its own complete at their client time.
+  struct Admission {
+    double time;
+    RequestId id;
+    int entry_layer;
+  };
+  std::vector<Admission> adm;
+  std::vector<double> client_done(n, -1.0);
+  std::vector<CompletionLocation> client_loc(n, CompletionLocation::server);
+  const bool collab = job.config.offload != OffloadMode::none;
+  if (collab) {
+    struct Recorder : StepHook {
+      std::vector<Admission>* adm = nullptr;
+      void admit(RequestId id, int, int entry_layer, Ms now) override { adm->push_back({now, id, entry_layer}); }
+    } rec;
+    rec.adm = &adm;
+    Simulator client_side(job.spec, job.ps, job.config, job.trace ? &*job.trace : nullptr,
+                          job.client ? &*job.client : nullptr);
+    client_side.set_hook(&rec);
+    const SimResult res = client_side.run();
+    std::vector<char> at_server(n + 1, 0);
+    for (const Admission& a : adm) at_server[static_cast<std::size_t>(a.id)] = 1;
+    for (const RequestOutcome& o : res.outcomes)
+      if (!at_server[static_cast<std::size_t>(o.id)] && !o.dropped) {
+        client_done[static_cast<std::size_t>(o.id - 1)] = o.completion;
+        client_loc[static_cast<std::size_t>(o.id - 1)] = o.location;
+      }
+    std::sort(adm.begin(), adm.end(),
+              [](const Admission& x, const Admission& y) { return x.time < y.time || (x.time == y.time && x.id < y.id); });
+  } else {
+    adm.reserve(n);
+    for (std::size_t i = 0; i < n; ++i) adm.push_back({arrivals[i].time, static_cast<RequestId>(i) + 1, 1});
+  }
+  const std::size_t n_adm = adm.size();
   std::vector<Book> book(n);
   std::vector<int> mix;
   if (job.spec.dnn_mix.empty()) {
@@ -116,6 +162,7 @@ json serve_live(Executor& ex, const json& j) {
   std::size_t ai = 0, resolved = 0;
   long n_steps = 0, n_plans = 0, h2d_bytes = 0, d2h_bytes = 0;
   double sched_ms = 0, max_sched_ms = 0;
+  double predicted_ms = 0;  // sum of the launched steps' table durations (what the scheduler assumed)
   double host_admit_ms = 0, host_step_ms = 0;  // host time in admissions / step issue (+ bookkeeping)
   const long launches0 = ex.launches();
   std::vector<int> step_batch_hist;
@@ -135,6 +182,18 @@ json serve_live(Executor& ex, const json& j) {
   };
   auto layer_shared = [&](int dnn, int layer) { return job.ps.layer_is_shared(dnn, layer); };
 
+  // Every request's generation-time facts; client-finished requests resolve
+  // at their client completion time.
+  for (std::size_t i = 0; i < n; ++i) {
+    Book& b = book[i];
+    b.dnn = mix[static_cast<std::size_t>(arrivals[i].dnn) % mix.size()];
+    b.arrival = arrivals[i].time;
+    b.deadline = deadlines ? arrivals[i].time + job.spec.relative_deadline : kNoDeadline;
+    if (client_done[i] >= 0) {
+      b.location = client_loc[i];
+      finish(static_cast<RequestId>(i) + 1, client_done[i]);
+    }
+  }
   ex.sync();
   cudaEvent_t dev0, dev1;
   cudaEventCreate(&dev0);
@@ -145,26 +204,25 @@ json serve_live(Executor& ex, const json& j) {
     double now = ms_since(t0);
     // 1. admissions
     const auto ha0 = Clock::now();
-    while (ai < n && arrivals[ai].time <= now) {
-      const RequestId id = static_cast<RequestId>(ai) + 1;
-      Book& b = book[ai];
-      b.dnn = mix[static_cast<std::size_t>(arrivals[ai].dnn) % mix.size()];
-      b.arrival = arrivals[ai].time;
-      b.deadline = deadlines ? arrivals[ai].time + job.spec.relative_deadline : kNoDeadline;
+    while (ai < n_adm && adm[ai].time <= now) {
+      const RequestId id = adm[ai].id;
+      const std::size_t i = static_cast<std::size_t>(id - 1);
+      Book& b = book[i];
       const int net = dnn_map[static_cast<std::size_t>(b.dnn)];
-      const int img = static_cast<int>(ai % static_cast<std::size_t>(pool));
-      if (h2d) {
+      const int img = static_cast<int>(i % static_cast<std::size_t>(pool));
+      if (h2d && adm[ai].entry_layer == 1) {
         ex.admit_rgb(id, net, host_pool[static_cast<std::size_t>(net)] + img_floats[static_cast<std::size_t>(net)] * img);
         h2d_bytes += static_cast<long>(img_floats[static_cast<std::size_t>(net)] * sizeof(float));
       } else {
-        ex.admit(id, net, 1, ex.pool_image(net, img), true);
+        ex.admit(id, net, adm[ai].entry_layer, ex.pool_image(net, img), true);
       }
       Request r;
       r.id = id;
       r.dnn = b.dnn;
       r.arrival = b.arrival;
       r.deadline = b.deadline;
-      r.layer = 1;
+      r.layer = adm[ai].entry_layer;
+      if (collab) r.origin = static_cast<int>((id - 1) % static_cast<RequestId>(job.config.clients));
       pending.insert(std::upper_bound(pending.begin(), pending.end(), r, arrives_before), r);
       ++arrivals_since;
       ++ai;
@@ -274,6 +332,7 @@ json serve_live(Executor& ex, const json& j) {
         ev_free.pop_back();
         cudaEventRecord(f.ev, ex.stream());
         f.expected_end = start_est + st.duration;
+        predicted_ms += st.duration;
         inflight.push_back(std::move(f));
         ++next_step;
         if (reschedule_trigger(true, arrivals_since > 0, crossed)) needs_schedule = true;
@@ -282,8 +341,8 @@ json serve_live(Executor& ex, const json& j) {
       }
     }
     // 4. idle: wait for the next event
-    if (inflight.empty() && pending.empty() && ai < n) {
-      const double wait = arrivals[ai].time - ms_since(t0);
+    if (inflight.empty() && pending.empty() && ai < n_adm) {
+      const double wait = adm[ai].time - ms_since(t0);
       if (wait > 0.2) std::this_thread::sleep_for(std::chrono::microseconds(static_cast<long>((wait - 0.1) * 1000)));
     }
   }
@@ -299,7 +358,7 @@ json serve_live(Executor& ex, const json& j) {
   // Outcomes (reference semantics: drops count against on-time).
   std::vector<RequestOutcome> outs(n);
   double first_arrival = n ? arrivals.front().time : 0, last_completion = 0;
-  int on_time_completed = 0;
+  int on_time_completed = 0, server_completed = 0;
   json top1 = json::array();
   for (std::size_t i = 0; i < n; ++i) {
     RequestOutcome& o = outs[i];
@@ -309,11 +368,17 @@ json serve_live(Executor& ex, const json& j) {
     o.arrival = b.arrival;
     o.deadline = b.deadline;
     o.dropped = b.dropped;
+    o.location = b.location;
     if (b.done) {
       o.completion = b.completion;
       o.on_time = b.deadline >= kNoDeadline || b.completion <= b.deadline;
       last_completion = std::max(last_completion, b.completion);
       if (o.on_time) ++on_time_completed;
+      if (b.location != CompletionLocation::server) {  // finished on its client: no server output
+        top1.push_back(-1);
+        continue;
+      }
+      ++server_completed;
       const float* p = results + i * classes;
       int best = 0;
       for (int c = 1; c < classes; ++c)
@@ -326,7 +391,8 @@ json serve_live(Executor& ex, const json& j) {
   json dumped = json::object();
   for (const auto& idj : j.value("dump_ids", json::array())) {
     const std::int64_t id = idj.get<std::int64_t>();
-    if (id >= 1 && static_cast<std::size_t>(id) <= n && book[static_cast<std::size_t>(id - 1)].done)
+    if (id >= 1 && static_cast<std::size_t>(id) <= n && book[static_cast<std::size_t>(id - 1)].done &&
+        book[static_cast<std::size_t>(id - 1)].location == CompletionLocation::server)
       dumped[std::to_string(id)] = std::vector<float>(results + (id - 1) * classes, results + id * classes);
   }
   cudaFreeHost(results);
@@ -342,6 +408,11 @@ json serve_live(Executor& ex, const json& j) {
   out["served_rps"] = span_s > 0 ? m.completed / span_s : 0.0;
   out["goodput_rps"] = span_s > 0 ? on_time_completed / span_s : 0.0;
   out["offered_rps"] = job.spec.rate;
+  out["server_completed"] = server_completed;
+  out["predicted_step_ms_total"] = predicted_ms;
+  out["server_admissions"] = n_adm;
+  out["admitted_mid_network"] = std::count_if(adm.begin(), adm.end(), [](const Admission& a) { return a.entry_layer > 1; });  // completed on the GPU (collab: excludes client-finished)
+  out["server_served_rps"] = span_s > 0 ? server_completed / span_s : 0.0;
   out["wall_ms"] = wall;
   out["host_admit_ms"] = host_admit_ms;
   out["host_step_ms"] = host_step_ms;
@@ -368,6 +439,11 @@ json serve_live(Executor& ex, const json& j) {
   out["d2h_bytes"] = d2h_bytes;
   out["top1"] = top1;
   out["probs"] = dumped;
+  if (!dumped.empty()) {  // suite network of every request (to check dumped outputs)
+    std::vector<int> nets(n);
+    for (std::size_t i = 0; i < n; ++i) nets[i] = dnn_map[static_cast<std::size_t>(book[i].dnn)];
+    out["dnn_of"] = nets;
+  }
   return out;
 }
 
@@ -381,6 +457,17 @@ json measure_profile(Executor& ex, const json& opts) {
   const bool flush = opts.value("flush_l2", false);
   json tuned = nullptr;
   if (opts.value("tune_tiles", false)) tuned = json::parse(ex.tune_tiles(batches, std::max(3, reps / 2)));
+  // "pass" (default): each layer's latency inside back-to-back passes of its
+  // network (what a multi-layer step costs); "layer": each layer alone,
+  // synchronised (adds launch latency and idle gaps per layer; the only mode
+  // with flush_l2, which needs an L2 flush before every timed layer).
+  const std::string timing = flush ? "layer" : opts.value("timing", std::string("pass"));
+  if (timing != "pass" && timing != "layer") throw std::invalid_argument("timing: pass | layer");
+  // pass timings of every net at every batch: [net][batch index][layer - 1]
+  std::vector<std::vector<std::vector<double>>> pass_ms(s.nets.size());
+  if (timing == "pass")
+    for (std::size_t i = 0; i < s.nets.size(); ++i)
+      for (int b : batches) pass_ms[i].push_back(ex.profile_pass(static_cast<int>(i), b, reps));
   json comps = json::array();
   for (std::size_t c = 0; c < s.components.size(); ++c) {
     // measure a component inside the first DNN that contains it
@@ -398,7 +485,12 @@ json measure_profile(Executor& ex, const json& opts) {
       const LayerDef& L = net->layers[static_cast<std::size_t>(k - 1)];
       if (L.component != static_cast<int>(c)) continue;
       json grid = json::array();
-      for (int b : batches) grid.push_back(json::array({b, ex.profile_layer(net_idx, k, b, reps, flush)}));
+      for (std::size_t bi = 0; bi < batches.size(); ++bi) {
+        const int b = batches[bi];
+        const double ms = timing == "pass" ? pass_ms[static_cast<std::size_t>(net_idx)][bi][static_cast<std::size_t>(k - 1)]
+                                           : ex.profile_layer(net_idx, k, b, reps, flush);
+        grid.push_back(json::array({b, ms}));
+      }
       const OpDef& last = net->ops[static_cast<std::size_t>(L.ops.back())];
       const long bits = 32L * last.Ho * std::max(last.Wo, 1) * last.out.C;
       layers.push_back({{"name", L.name}, {"output_bits", bits}, {"runtime_ms", grid}});
@@ -412,7 +504,8 @@ json measure_profile(Executor& ex, const json& opts) {
     dnns.push_back({{"id", n.name}, {"stages", stages}});
   }
   json prof = {{"max_batch", ex.max_batch()}, {"components", comps}, {"dnns", dnns}};
-  if (!tuned.is_null()) prof["tile_tune"] = tuned;  // [op, batch, ms wide, ms narrow] (extra key; opt-in)
+  if (!tuned.is_null()) prof["tile_tune"] = tuned;  // [op, batch, choice, layer ms] (extra key; opt-in)
+  prof["timing"] = timing;                          // extra key (ignored by the profile parsers)
   return prof;
 }
 

@@ -60,7 +60,20 @@ def shard_job(job: dict, world: int, rank: int, policy: str = "round_robin") -> 
     w = job["workload"]
     arr = bs.generate_arrivals(w.get("process", "poisson"), w.get("rate", 100.0), w.get("count", 5000),
                                w.get("seed", 1), w.get("dnn_mix"))
-    sh = shard(arr, world, rank, policy, job.get("sim", {}).get("clients", 0))
+    sim = job.get("sim", {})
+    clients = sim.get("clients", 0)
+    sh = shard(arr, world, rank, policy, clients)
     wl = {k: v for k, v in w.items() if k not in ("process", "rate", "count")}
     wl["explicit_arrivals"] = [[bs.bits64(t), d, b] for t, d, b in sh.arrivals]
-    return dict(job, workload=wl), sh
+    out = dict(job, workload=wl)
+    if clients:
+        # Collaborative mode: with clients % world == 0, by-client routing
+        # (and round robin) hands shard r the global ids r + world m, i.e.
+        # the global clients r, r + world, ...; the shard's own renumbered ids
+        # then map to local client (j - 1) % (clients / world) = global
+        # client // world, so every request keeps its client's queue and
+        # uplink history (reference simulator.hpp:297).
+        if clients % world or policy == "dnn_affine":
+            raise ValueError("collaborative sharding needs clients % world == 0 and by-client routing")
+        out["sim"] = dict(sim, clients=clients // world)
+    return out, sh

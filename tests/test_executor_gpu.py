@@ -358,3 +358,74 @@ def test_bf16_path_tolerance_and_top1(suite):
     assert r["err_vs_bf16_emulation"] < 0.75 * r["emulation_err_vs_fp32"]
     assert r["top1_agreement_vs_bf16_emulation"] >= 0.9
     assert r["err_vs_fp32"] < 0.25
+
+
+def _check_live_outputs(ex, r, image_seed, pool, orcs, limit=6):
+    """Dumped live-serving probabilities of completed requests against the
+    CPU oracle (image of request id = pool image (id - 1) % pool)."""
+    from paper_2304_09961_b200.executor import make_image
+    checked = 0
+    for sid, probs in sorted(r["probs"].items(), key=lambda kv: int(kv[0]))[:limit]:
+        rid = int(sid)
+        dnn = r["dnn_of"][rid - 1] if "dnn_of" in r else 0
+        n = ex.desc["nets"][dnn]
+        img = make_image(image_seed, (rid - 1) % pool, n["in_H"], n["in_W"], n["in_C"])
+        orc = orcs[dnn]
+        assert_request_matches(np.asarray(probs, np.float32), orc.probs(orc.forward(img)), TOL)
+        checked += 1
+    return checked
+
+
+def test_live_serve_h2d_outputs_match_oracle():
+    """The headline e2e path: live serving with every image copied H2D from
+    pinned host memory (packed RGB, expanded on the device), the batched
+    retire into pinned memory -- served probabilities match the oracle."""
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("googlenet", max_batch=90, max_requests=512) as ex:
+        prof = ex.profile_table(batches=(1, 8, 32, 90), reps=3)
+        t1 = sum(L["runtime_ms"][0][1] for L in prof["components"][0]["layers"])
+        pool = 8
+        job = {"profile": prof, "workload": {"process": "poisson", "rate": 3000, "count": 200, "seed": 5,
+                                             "relative_deadline": 20 * t1},
+               "sim": {"scheduler": "ours-tardy", "granularity": "layer"}, "image_pool": pool, "image_seed": 4,
+               "h2d": True, "dump_ids": list(range(1, 201))}
+        r = ex.serve(job)
+        assert r["completed"] + r["dropped"] == 200 and r["h2d_bytes"] > 0
+        orc = NetOracle(ex.desc, 0, ex.weights())
+        assert _check_live_outputs(ex, r, 4, pool, [orc]) >= 4
+
+
+def test_live_serve_collab_config5():
+    """Config 5 served live: the client side (compute queues, uplink trace,
+    partial-offload decisions) replayed in virtual time by the reference-
+    semantics simulator; the server admits its requests at their entry layer
+    (client prefix emulated on the side stream) and serves the suffix on the
+    wall clock; GPU outputs of mid-network admissions match the oracle.
+    The table is the slow synthetic one of the replay test: on the measured
+    B200 table the server is so much faster than the Jetson client that the
+    offload decision sends every raw input (entry layer 1)."""
+    import os
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("collab", max_batch=90, max_requests=256) as ex:
+        names = [n["name"] for n in ex.desc["nets"]]
+        prof = synth_profile(ex, 1.0, 0.02)
+        pool = 8
+        job = {"profile": prof,
+               "workload": {"process": "pareto", "rate": 60, "count": 120, "seed": 11,
+                            "relative_deadline": 300.0, "dnn_mix": [[n, 0.5] for n in names]},
+               "sim": {"scheduler": "ours-time", "granularity": "group", "max_batch": 90,
+                       "offload": "partial", "clients": 16},
+               "client_profile": "tests/golden/ref_data/jetson_nano.json",
+               "trace": "tests/golden/ref_data/lte_uplink.csv", "trace_scale": 10.0,
+               "image_pool": pool, "image_seed": 9, "dump_ids": list(range(1, 121))}
+        cwd = os.getcwd()
+        os.chdir(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        try:
+            r = ex.serve(job)
+        finally:
+            os.chdir(cwd)
+        assert r["completed"] + r["dropped"] == 120
+        assert r["admitted_mid_network"] > 0 and r["server_completed"] > 0
+        w = ex.weights()
+        orcs = [NetOracle(ex.desc, k, w) for k in range(len(names))]
+        assert _check_live_outputs(ex, r, 9, pool, orcs) >= 3

@@ -82,3 +82,34 @@ def test_by_client_keeps_client_map():
     owners = route(arr, 4, "by_client", clients=8)
     for gid, o in enumerate(owners, start=1):
         assert o == ((gid - 1) % 8) % 4
+
+
+def test_collab_by_client_sharding_keeps_client_map():
+    """Config 5 across GPUs: by-client routing with clients % world == 0
+    hands each shard whole clients, and the shard's renumbered ids map to
+    local client (j - 1) % (clients / world) == global client // world, so
+    every request keeps its client (reference simulator.hpp:297). The shard
+    jobs run through the bit-exact simulator with their local client count."""
+    from paper_2304_09961_b200._native import host_call
+    from paper_2304_09961_b200.shard import shard_job
+    job = {"job": "sim", "profile": "tests/golden/ref_data/five_dnns.json",
+           "workload": {"process": "pareto", "rate": 120, "count": 240, "seed": 5, "relative_deadline": 150,
+                        "dnn_mix": [["vgg16", .5], ["fcn", .5]]},
+           "sim": {"scheduler": "ours-tardy", "granularity": "group", "offload": "partial", "clients": 12},
+           "trace": "tests/golden/ref_data/lte_uplink.csv", "trace_scale": 10,
+           "client_profile": "tests/golden/ref_data/jetson_nano.json"}
+    os.chdir(ROOT)
+    world, clients = 4, 12
+    seen = set()
+    for rank in range(world):
+        sj, sh = shard_job(job, world, rank, "by_client")
+        assert sj["sim"]["clients"] == clients // world
+        for j, gid in enumerate(sh.global_ids, start=1):
+            assert ((gid - 1) % clients) // world == (j - 1) % (clients // world)
+            assert ((gid - 1) % clients) % world == rank
+        seen.update(sh.global_ids)
+        lines = host_call(sj).splitlines()
+        assert json.loads(lines[-1])["generated"] == len(sh.global_ids)
+    assert seen == set(range(1, 241))
+    with pytest.raises(ValueError):
+        shard_job(job, 5, 0, "by_client")

@@ -48,6 +48,7 @@ for proc in ([cfg["process"], "poisson"] if cfg["process"] != "poisson" else ["p
         ex.stats(False)
         busy = sum(v["ms"] for v in s.values() if isinstance(v, dict) and "ms" in v)
         keep = {k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items() if not isinstance(v, (list, dict)) or k == "step_members_hist"}
+        keep["kernel_over_predicted"] = round(busy / max(r["predicted_step_ms_total"], 1e-9), 3)
         keep["kernel_ms"] = round(busy, 2)
         keep["busy_frac"] = round(busy / max(r["device_ms"], 1e-9), 3)
         print(proc, "deadline", deadline, json.dumps(keep), flush=True)
