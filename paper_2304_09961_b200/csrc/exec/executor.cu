@@ -29,14 +29,15 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
     : suite_(build_suite(suite_name)), device_(device), max_batch_(max_batch) {
   ck(cudaSetDevice(device), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
-  // Admission stream at the highest priority: its expand kernels are tiny
-  // and gate the next steps (ready events); at high load the serving
-  // stream's persistent kernels otherwise keep them waiting for SMs.
+  // Admission and client-prefix streams at the highest priority: their
+  // kernels are small and gate the next steps (ready events); at high load the
+  // serving stream's persistent kernels -- and, with PDL, the next kernel's
+  // CTAs parked in griddepcontrol.wait -- otherwise keep them waiting for SMs.
   {
     int lo = 0, hi = 0;
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
     ck(cudaStreamCreateWithPriority(&copy_, cudaStreamNonBlocking, hi), "copy stream");
+    ck(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, hi), "side stream");
   }
   ck(cudaMalloc(&d_weights_, suite_.weights.size() * sizeof(float)), "weights");
   ck(cudaMemcpy(d_weights_, suite_.weights.data(), suite_.weights.size() * sizeof(float), cudaMemcpyHostToDevice),

@@ -125,6 +125,7 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
       CK(cudaMemset(trace, 0, 8 * 3600));
     }
     CK(launch_conv_tc(p, 0));
+    if (trace && std::getenv("BS_CONV_TRACE")[0] == '2') CK(launch_conv_tc(p, 0));  // trace the 2nd of a pair
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_host, dout, out_img * nimg * sizeof(float), cudaMemcpyDeviceToHost));
     if (trace) {
@@ -148,17 +149,20 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
           std::fprintf(stderr, "  cta %3d start %7lld setup %7lld firstA %7lld end %7lld\n", b, rel(h[8 + 4 * b]),
                        rel(h[9 + 4 * b]), rel(h[10 + 4 * b]), rel(h[11 + 4 * b]));
       for (int it = 0; it < 48 && h[1024 + it * 5 + 4]; ++it)
-        std::fprintf(stderr, "  it %2d A %7lld B %7lld landed %7lld split %7lld mma %7lld | cvt %7lld slot %7lld st %7lld wst %7lld\n", it,
+        std::fprintf(stderr, "  it %2d A %7lld B %7lld landed %7lld split %7lld mma %7lld | ta_ok %7lld b_ok %7lld\n", it,
                      rel(h[1024 + it * 5]), rel(h[1025 + it * 5]), rel(h[1026 + it * 5]), rel(h[1027 + it * 5]),
-                     rel(h[1028 + it * 5]), rel(h[2048 + it * 4]), rel(h[2049 + it * 4]), rel(h[2050 + it * 4]),
-                     rel(h[2051 + it * 4]));
+                     rel(h[1028 + it * 5]), rel(h[2048 + it * 4]), rel(h[2049 + it * 4]));
       for (int j = 0; j < 32 && h[3072 + j * 8]; ++j)
         std::fprintf(stderr, "  unit %2d epi wait %7lld acc_full %7lld chunks %7lld %7lld %7lld %7lld\n", j,
                      rel(h[3072 + j * 8]), rel(h[3073 + j * 8]), rel(h[3074 + j * 8]), rel(h[3075 + j * 8]),
                      rel(h[3076 + j * 8]), rel(h[3077 + j * 8]));
+      for (int c = 0; c < 2 && h[3300 + c * 8]; ++c)
+        std::fprintf(stderr, "  epi chunk %d: start %7lld tmem_ld %7lld staged %7lld bias %7lld stored %7lld\n", c,
+                     rel(h[3300 + c * 8]), rel(h[3301 + c * 8]), rel(h[3302 + c * 8]), rel(h[3303 + c * 8]),
+                     rel(h[3304 + c * 8]));
       for (int j = 0; j < 32 && h[3400 + j * 4]; ++j)
-        std::fprintf(stderr, "  producer unit %2d top %7lld setup %7lld\n", j, rel(h[3400 + j * 4]),
-                     rel(h[3401 + j * 4]));
+        std::fprintf(stderr, "  producer unit %2d top %7lld ptrs %7lld tap %7lld | b-warp loop entry %7lld\n", j,
+                     rel(h[3400 + j * 4]), rel(h[3401 + j * 4]), rel(h[3402 + j * 4]), rel(h[3403]));
       p.trace = nullptr;
       cudaFree(trace);
     }

@@ -37,6 +37,7 @@
 // 8 MMA issuer (+ TMEM owner), 9 B TMA issuer, 10-13 A converters (group 0),
 // 14 idle, 15-18 A converters (group 1).
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <type_traits>
 
@@ -297,7 +298,6 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
   const uint32_t smem_base = ptx::smem_u32(smem);
   // trace: [8 + 4 b + {0 start, 1 setup done, 2 first A issued, 3 end}]
   if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x] = gtime();
-  pdl::launch_dependents();  // pdl.cuh: the next layer kernel may be scheduled
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RA; ++s) {
@@ -327,11 +327,17 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // Everything above overlapped the previous kernel's tail (PDL). The weight
-  // TMA warp reads only immutable weights and starts at once; every other
-  // role touches activations / blob tables and waits
-  // for the previous kernel to complete.
-  if (warp != 9) pdl::wait();
+  // Everything above overlapped the previous kernel's tail (PDL). Only the
+  // roles that read activations wait for the previous kernel: the A gather
+  // (here) and the epilogue (after it has prefetched its immutable blob-table
+  // entries and bias, before residual reads). The weight TMA warp reads only
+  // immutable weights; the MMA issuer and the converters touch shared memory
+  // and TMEM only, fed by those roles, so they start at once. Every output
+  // store follows the gather's wait (it depends on the gathered A), and the
+  // kernel cannot complete before its producers passed the wait, so
+  // completion stays ordered along the stream. The gather waits right
+  // before its first copy, so its first unit's row setup and blob-table loads
+  // (immutable for the kernel) overlap the previous kernel too.
   if (p.trace && threadIdx.x == 0) p.trace[8 + 4 * blockIdx.x + 1] = gtime();
 
   // Converter: thread = one A row (TMEM lane). Reads its 128-byte row of a
@@ -385,6 +391,11 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
     const int HoWo = p.Ho * p.Wo;
     const float* dummy = p.wgt;
     int it = 0;  // ring position across units
+    bool waited = false;
+    auto wait_once = [&] {
+      if (!waited) pdl::wait();
+      waited = true;
+    };
     // (image, ho, wo) of rows r0 + 16 i of the tile at m_base: one division
     // pair, then a 16-row walk (was 16 divisions per unit; the unit switch
     // stalled the stem's producer ~1.4 us). Rows past M: ok = false, image 0.
@@ -464,6 +475,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
           ok_w[i] = rok && kw < p.KW && wi >= 0 && wi < p.W;
           base[i] = img + (static_cast<long>(h0[i]) * p.W + wi) * p.in_ldc + ci;
         }
+        wait_once();
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % RA;
           if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
@@ -487,6 +499,9 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
       BS_UNIT_PROBLEM(u)
       const bool aligned = p.Cin % kBK == 0;
       const Unit w = unit_of(p, lu, BN, KT);
+      const bool ptr_tr = p.trace && t == 0 && blockIdx.x == 0 && u < 32 * static_cast<int>(gridDim.x);
+      const int ptr_j = u / static_cast<int>(gridDim.x);
+      if (ptr_tr) p.trace[3400 + ptr_j * 4 + 0] = gtime();
       const float* row_base[8];
       int row_h[8], row_w[8];
       bool row_ok[8];
@@ -500,6 +515,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
           row_base[i] = p.in_ptrs[rn[i]] + p.in_off;
         }
       }
+      if (ptr_tr) p.trace[3400 + ptr_j * 4 + 1] = gtime() + (reinterpret_cast<uintptr_t>(row_base[0]) & 1);
       uint32_t doff[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) doff[i] = swz(r0 + 16 * i, c);
@@ -522,6 +538,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
           }
         };
         set_tap();
+        if (ptr_tr) p.trace[3400 + ptr_j * 4 + 2] = gtime() + (nbytes[7] & 1);
+        wait_once();
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % RA;
           if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
@@ -556,6 +574,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
         int ci = k0 - q * p.Cin;
         int kh = q / p.KW;
         int kw = q - kh * p.KW;
+        wait_once();
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % RA;
           if (it >= RA) ptx::mbar_wait(&ra_empty[s], ((it / RA) - 1) & 1);
@@ -588,6 +607,13 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
         }
       }
     }
+    wait_once();  // (every CTA has >= 1 unit; kept so completion order never depends on it)
+    // The next kernel may be scheduled once every CTA has issued its last
+    // gather (its prologue then overlaps this CTA's last K tiles and
+    // epilogue). Triggering at entry let a whole step's kernels become
+    // resident at once, parked in griddepcontrol.wait, and starve the other
+    // streams' kernels (admission, client prefixes) of SMs.
+    pdl::launch_dependents();
   } else if (warp < 8) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;
@@ -623,6 +649,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
       ptx::cp_async_commit();
     };
     if (static_cast<int>(blockIdx.x) < units) prefetch(blockIdx.x, 0);
+    pdl::wait();  // residual rows (L1 prefetch / loads) come from earlier kernels
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       BS_UNIT_PROBLEM(u)
@@ -704,9 +731,12 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
               rv[rq] = ok ? __ldg(reinterpret_cast<const float4*>(rr + nc)) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
+          const bool ctr = etr && j == 0 && jj < 2;
+          if (ctr) p.trace[3300 + jj * 8 + 0] = gtime();
           uint32_t v[32];
           ptx::tmem_ld32(tbase + jj * 32, v);
           ptx::tmem_ld_wait();
+          if (ctr) p.trace[3300 + jj * 8 + 1] = gtime() + (v[31] & 1);
           if (jj == BN / 32 - 1) {
             ptx::tc_fence_before();
             ptx::mbar_arrive(&acc_empty[acc]);  // TMEM buffer free for unit j + kAcc
@@ -719,6 +749,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
                         make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
                                     __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
           __syncwarp();
+          if (ctr) p.trace[3300 + jj * 8 + 2] = gtime();
           const int cq = lane & 7;          // 16-byte chunk of the row segment
           const int nc = n0 + cq * 4;       // first column of the chunk
           const bool col_ok = nc < p.N;
@@ -726,37 +757,45 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
           // Zero past N (the prefetch stored 0 there), so no test is needed.
           const float4 b4 = *reinterpret_cast<const float4*>(bias_st + jj * 32 + cq * 4);
           if (fast) {
-            // Branch-free rows: batched LDS (plain loads, reorderable), bias,
-            // activation as a compile-time clamp, st.global.v4.
             const float* st = reinterpret_cast<const float*>(smem + S::kStagingOffset + ew * 32 * 128);
-            auto rows = [&](auto relu_tag) {
-              constexpr int RELU = decltype(relu_tag)::value;
+            // Rows in batches of RB: all staging / row-pointer loads of a
+            // batch are issued before the first use, so their shared-memory
+            // latencies overlap (one dependent LDS chain per row cost ~60
+            // cycles x 8 rows per chunk before). The activation is a runtime
+            // clamp (one code copy instead of one per activation kind).
+            const float lo = p.relu ? 0.f : -INFINITY, hi = p.relu == 2 ? 6.f : INFINITY;
+            constexpr int RB = RES ? 4 : 8;
+            if (ctr) p.trace[3300 + jj * 8 + 3] = gtime();
 #pragma unroll
-              for (int rq = 0; rq < 8; ++rq) {
-                const int rl = rq * 4 + (lane >> 3);
-                float4 x = *reinterpret_cast<const float4*>(st + rl * 32 + ((cq ^ (rl & 7)) << 2));
-                x.x += b4.x; x.y += b4.y; x.z += b4.z; x.w += b4.w;
-                if constexpr (RES) {
-                  x.x += rv[rq].x; x.y += rv[rq].y; x.z += rv[rq].z; x.w += rv[rq].w;
-                }
-                if constexpr (RELU >= 1) {
-                  x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
-                }
-                if constexpr (RELU == 2) {
-                  x.x = fminf(x.x, 6.f); x.y = fminf(x.y, 6.f); x.z = fminf(x.z, 6.f); x.w = fminf(x.w, 6.f);
-                }
-                if (p.round_out) {
-                  x.x = ptx::round_tf32(x.x); x.y = ptx::round_tf32(x.y);
-                  x.z = ptx::round_tf32(x.z); x.w = ptx::round_tf32(x.w);
-                }
-                const unsigned long long op = fin_out[rl];
-                if (op && col_ok) ptx::stg128(reinterpret_cast<float*>(op) + nc, x);
+            for (int g = 0; g < 8; g += RB) {
+              float4 x[RB];
+              unsigned long long o[RB];
+#pragma unroll
+              for (int i = 0; i < RB; ++i) {
+                const int rl = (g + i) * 4 + (lane >> 3);
+                x[i] = *reinterpret_cast<const float4*>(st + rl * 32 + ((cq ^ (rl & 7)) << 2));
+                o[i] = fin_out[rl];
               }
-            };
-            if (p.relu == 1) rows(std::integral_constant<int, 1>{});
-            else if (p.relu == 2) rows(std::integral_constant<int, 2>{});
-            else rows(std::integral_constant<int, 0>{});
+#pragma unroll
+              for (int i = 0; i < RB; ++i) {
+                float4& y = x[i];
+                y.x += b4.x; y.y += b4.y; y.z += b4.z; y.w += b4.w;
+                if constexpr (RES) {
+                  y.x += rv[g + i].x; y.y += rv[g + i].y; y.z += rv[g + i].z; y.w += rv[g + i].w;
+                }
+                y.x = fminf(fmaxf(y.x, lo), hi); y.y = fminf(fmaxf(y.y, lo), hi);
+                y.z = fminf(fmaxf(y.z, lo), hi); y.w = fminf(fmaxf(y.w, lo), hi);
+                if (p.round_out) {
+                  y.x = ptx::round_tf32(y.x); y.y = ptx::round_tf32(y.y);
+                  y.z = ptx::round_tf32(y.z); y.w = ptx::round_tf32(y.w);
+                }
+              }
+#pragma unroll
+              for (int i = 0; i < RB; ++i)
+                if (o[i] && col_ok) ptx::stg128(reinterpret_cast<float*>(o[i]) + nc, x[i]);
+            }
             __syncwarp();
+            if (ctr) p.trace[3300 + jj * 8 + 4] = gtime();
             return;
           }
           auto store_row = [&](int rq, const float4& r4) {
@@ -850,7 +889,9 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
       for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
         const int sa = it % TA, sb = it % NB;
         ptx::mbar_wait(&ta_full[sa], (it / TA) & 1);
+        if (p.trace && lane == 0 && blockIdx.x == 0 && it < 48) p.trace[2048 + it * 4 + 0] = gtime();
         ptx::mbar_wait(&b_full[sb], (it / NB) & 1);
+        if (p.trace && lane == 0 && blockIdx.x == 0 && it < 48) p.trace[2048 + it * 4 + 1] = gtime();
         ptx::tc_fence_after();
         if (p.trace && lane == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 4] = gtime();
         if (ptx::elect_one()) {
@@ -882,6 +923,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
     // ------------------------------------------------------------ B TMA
     if (lane == 0) {
       int it = 0;
+      if (p.trace && blockIdx.x == 0) p.trace[3400 + 3] = gtime();
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         BS_UNIT_PROBLEM(u)
         const Unit w = unit_of(p, lu, BN, KT);

@@ -5,9 +5,12 @@
 // prologue -- barrier init, TMEM allocation, tensor-map prefetch, weight
 // loads -- on SMs that k has released) and park in griddepcontrol.wait until
 // k has completed and its memory is visible. Rules that keep this exact:
-//   * every kernel issues launch_dependents() at entry, by every CTA, so a
-//     dependent grid is only scheduled once all CTAs of the current grid are
-//     resident (dependents can never starve it of SMs);
+//   * every kernel issues launch_dependents() in every CTA, so a dependent
+//     grid is only scheduled once all CTAs of the current grid are resident
+//     (dependents can never starve it of SMs). The conv kernel triggers after
+//     its last gather, not at entry: entry triggers let every kernel of a
+//     step become resident at once (each parked in griddepcontrol.wait) and
+//     starve other streams of SMs;
 //   * every kernel calls wait() before it reads or writes anything another
 //     kernel produces or consumes (activations, blob tables, split-K
 //     workspace); only immutable inputs (weights, bias) may be touched before.
@@ -15,13 +18,14 @@
 //     kernel k+2 transitively sees kernel k.
 // Outside a PDL launch both instructions are no-ops.
 //
-// Opt-in (BS_PDL=1). Measured on B200: per-layer timings improve at small
-// batches (GoogLeNet b=8 layer sum 919 -> 853 us, b=90 unchanged), and with
-// the admission stream at the highest priority config 2 serves the same
-// with it (37.0k / e2e 36.5k req/s), but config 3 (shared-layer riders,
-// ride copies between kernels) drops from 2.5k to 1.4-1.5k req/s with PDL
-// even with no programmatic launch behind a copy, so the default launch
-// stays stream-serialised.
+// On by default (BS_PDL=0 disables). Measured on B200 (profiles/r02/pdl/):
+// whole-network passes GoogLeNet b=1 360 -> 252 us, ResNet-50 b=1 765 -> 557
+// us, GoogLeNet b=8 509 -> 412 us, b=90 unchanged; config 2 serves the same
+// (the latency table's T1 drops 0.42 -> 0.37 ms). The two Pareto configs (3,
+// 5) serve less on time with it: their schedulers plan on the faster
+// small-batch table and pick smaller steps (config 3 at 4000 req/s: mean
+// step 5.7 vs 8.2 requests), which lowers throughput under bursts; bench.py
+// runs those two with BS_PDL=0 and says so in the line.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -40,7 +44,7 @@ __device__ __forceinline__ void wait() { asm volatile("griddepcontrol.wait;" :::
 inline bool enabled() {
   static const bool on = [] {
     const char* e = std::getenv("BS_PDL");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }
