@@ -102,8 +102,8 @@ namespace conv_tc {
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // fp32 elements per 128-byte K row
 
-// Pipeline geometry per N tile. Three rings decouple the stages so no load
-// waits on an MMA it does not feed:
+// Pipeline geometry per N tile (TF32 / BF16). Three rings decouple the
+// stages so no load waits on an MMA it does not feed:
 //   raw A  (smem, RA x 16 KB): cp.async gather target; freed as soon as the
 //          converter warps have read a stage (not when the MMA finishes);
 //   B      (smem, NB x BN*128 B): weights by TMA, 128B-swizzled for UMMA
@@ -113,14 +113,26 @@ constexpr int kBK = 32;  // fp32 elements per 128-byte K row
 //          memory only serves B to the tensor core.
 // PREC: 0 = TF32 (one MMA), 1 = 2xTF32 (split A, ~fp32 accuracy),
 //       2 = BF16 (A rounded to bf16 by the converters, bf16 weights).
+// 2xTF32 ("HIS", hi in shared memory): the tensor core reads fp32 data as
+// TF32 by dropping the 13 low mantissa bits, i.e. exactly A_hi, so the A_hi
+// MMAs read the raw gathered stage from shared memory (SS form, the same
+// 128B-swizzled K-major layout as the weights) and only A_lo = A - A_hi goes
+// through the converters into TMEM (TS form). The A_hi MMAs need no
+// conversion, the converters and TMEM stores do half the work, and raw A,
+// B and the A_lo slot of a K tile live in one ring of D stages freed by the
+// K tile's single commit.
+
 template <int BN, int PREC>
 struct Cfg {
   static constexpr int kThreads = 608;
+  // 2xTF32 reads A_hi straight from the raw gathered stage (HIS, see below).
+  static constexpr bool HIS = PREC == 1;
   // BN = 256: one accumulator (256 columns) so the A slots still fit in TMEM;
   // the raw A ring shrinks to make room for the 32 KB B stages.
   static constexpr int kAcc = BN == 256 ? 1 : 2;                 // TMEM accumulator buffers
-  static constexpr int RA = BN == 32 ? 10 : BN == 256 ? 6 : 8;
-  static constexpr int kACols = PREC == 1 ? 2 * kBK : PREC == 2 ? kBK / 2 : kBK;  // TMEM columns per A slot
+  // TMEM columns per A slot: A_lo only for 2xTF32 (A_hi is read from shared
+  // memory), TF32 operand for TF32, packed bf16 pairs for BF16.
+  static constexpr int kACols = PREC == 2 ? kBK / 2 : kBK;
   static constexpr int kTA0 = kAcc * BN;                         // first A column (after the accumulators)
   // One operand stage = (TMEM A slot, B smem stage), released by a single
   // tcgen05.commit per K tile (each commit costs the tensor pipe ~84 cycles).
@@ -129,11 +141,16 @@ struct Cfg {
   // residual) and the unit's final row pointers [32] (out, residual).
   static constexpr int kEpiWarpBytes = 8 * BN + 1536;
   static constexpr int kBRow = PREC == 2 ? 64 : 128;             // bytes per weight row of a K tile
-  static constexpr int kNBmax = (232448 - 1024 - 512 - RA * kBM * 128 - kBM * 32 * 4 - 4 * kEpiWarpBytes) / (BN * kBRow);
-  static constexpr int TA = kTAmax < kNBmax ? (kTAmax < 8 ? kTAmax : 8) : (kNBmax < 8 ? kNBmax : 8);
-  static constexpr int NB = TA;
+  static constexpr int kFixed = 1024 + 512 + kBM * 32 * 4 + 4 * kEpiWarpBytes;
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * kBRow;
+  static constexpr int min3(int a, int b, int c) { return a < b ? (a < c ? a : c) : (b < c ? b : c); }
+  // HIS: one ring of D stages (raw A, B, TMEM A_lo) freed by one commit.
+  static constexpr int kD = min3(kTAmax, (232448 - kFixed) / (kABytes + kBBytes), 8);
+  static constexpr int RA = HIS ? kD : (BN == 32 ? 10 : BN == 256 ? 6 : 8);
+  static constexpr int kNBmax = (232448 - kFixed - RA * kABytes) / kBBytes;
+  static constexpr int TA = HIS ? kD : min3(kTAmax, kNBmax, 8);
+  static constexpr int NB = TA;
   static constexpr int kBOffset = RA * kABytes;
   static constexpr int kStagingOffset = kBOffset + NB * kBBytes;  // epilogue staging, 128 x 32 fp32
   static constexpr int kEpiOffset = kStagingOffset + kBM * 32 * 4;
@@ -141,6 +158,7 @@ struct Cfg {
   static constexpr int kTotal = kBarOffset + 512 + 1024;        // barriers + alignment slack
   static_assert(kTotal <= 232448, "shared memory budget");
   static_assert(TA >= 2, "TMEM budget");
+  static_assert(!HIS || (RA == TA && NB == TA), "HIS rings share one index");
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -276,7 +294,7 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
   uint64_t* b_full = ra_empty + RA;
   uint64_t* ta_full = b_full + NB;
   uint64_t* ta_empty = ta_full + TA;
-  uint64_t* b_empty = ta_empty;        // same ring: one commit frees slot and stage
+  uint64_t* b_empty = S::HIS ? ra_empty : ta_empty;  // same ring: one commit frees slot and stage(s)
   uint64_t* acc_full = ta_empty + TA;  // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
@@ -301,9 +319,10 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RA; ++s) {
-      // one cp.async .noinc arrival per producer thread
+      // one cp.async .noinc arrival per producer thread; freed by the
+      // converters' reads (TF32 / BF16) or by the K tile's commit (HIS)
       ptx::mbar_init(&ra_full[s], 128);
-      ptx::mbar_init(&ra_empty[s], 128);
+      ptx::mbar_init(&ra_empty[s], S::HIS ? 1 : 128);
     }
     for (int s = 0; s < NB; ++s) {
       ptx::mbar_init(&b_full[s], 1);
@@ -365,15 +384,30 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
         float4 v[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) v[c] = ptx::lds128(a_raw + roff[c]);
-        ptx::mbar_arrive(&ra_empty[s]);
-        uint32_t hi[32];
-        [[maybe_unused]] uint32_t lo[32];
-        a_operand<PREC>(v, hi, lo);
         const int sa = it % TA;
-        if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t dst = lane_base + sa * S::kACols;
-        a_store<PREC>(dst, hi, lo);
+        if constexpr (S::HIS) {
+          // A_lo only. Slot sa (== s) is free: this stage's gather was issued
+          // after the commit of K tile it - D, which retired the slot's MMAs.
+          uint32_t lo[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float x[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              lo[4 * c + e] = __float_as_uint(x[e] - __uint_as_float(__float_as_uint(x[e]) & 0xffffe000u));
+          }
+          ptx::tc_fence_after();
+          ptx::tmem_st32(lane_base + sa * S::kACols, lo);
+        } else {
+          ptx::mbar_arrive(&ra_empty[s]);
+          uint32_t hi[32];
+          [[maybe_unused]] uint32_t lo[32];
+          a_operand<PREC>(v, hi, lo);
+          if (it >= TA) ptx::mbar_wait(&ta_empty[sa], ((it / TA) - 1) & 1);
+          ptx::tc_fence_after();
+          const uint32_t dst = lane_base + sa * S::kACols;
+          a_store<PREC>(dst, hi, lo);
+        }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&ta_full[sa]);
@@ -888,6 +922,34 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
         const int sa = it % TA, sb = it % NB;
+        if constexpr (S::HIS) {
+          // A_hi = the raw stage read as TF32 (SS form), as soon as the
+          // gather and the weights have landed; then A_lo from TMEM (TS).
+          ptx::mbar_wait(&ra_full[sa], (it / TA) & 1);
+          ptx::mbar_wait(&b_full[sb], (it / NB) & 1);
+          ptx::fence_proxy_async_smem();  // cp.async (generic proxy) data -> tensor core (async proxy)
+          ptx::tc_fence_after();
+          if (p.trace && lane == 0 && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 4] = gtime();
+          const uint64_t a_desc = ptx::sw128_kmajor_desc(smem_base + sa * S::kABytes);
+          const uint64_t b_desc = ptx::sw128_kmajor_desc(smem_base + S::kBOffset + sb * S::kBBytes);
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int k = 0; k < kBK / 8; ++k)
+              ptx::mma_tf32(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
+          }
+          __syncwarp();
+          ptx::mbar_wait(&ta_full[sa], (it / TA) & 1);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            const uint32_t a_slot = a_tmem0 + sa * S::kACols;
+#pragma unroll
+            for (int k = 0; k < kBK / 8; ++k) ptx::mma_tf32_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, 1);
+            ptx::mma_commit(&ra_empty[sa]);  // frees raw stage, B stage and A_lo slot
+            if (kt == w.kt1 - 1) ptx::mma_commit(&acc_full[acc]);
+          }
+          __syncwarp();
+          continue;
+        }
         ptx::mbar_wait(&ta_full[sa], (it / TA) & 1);
         if (p.trace && lane == 0 && blockIdx.x == 0 && it < 48) p.trace[2048 + it * 4 + 0] = gtime();
         ptx::mbar_wait(&b_full[sb], (it / NB) & 1);
@@ -909,8 +971,6 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
             for (int k = 0; k < kBK / 8; ++k) {
               // A: 8 TMEM columns per K=8 step; B: +32 bytes inside the swizzled row.
               ptx::mma_tf32_ts(d_tmem, a_slot + 8 * k, b_desc + 2 * k, idesc, (kt != w.kt0) || k != 0);
-              if constexpr (SPLIT)
-                ptx::mma_tf32_ts(d_tmem, a_slot + kBK + 8 * k, b_desc + 2 * k, idesc, 1);
             }
           }
           ptx::mma_commit(&ta_empty[sa]);  // == b_empty[sb]

@@ -91,6 +91,12 @@ CASES = [
     dict(nimg=3, H=30, W=30, Cin=8, N=48, KH=3, KW=3, stride=1, pad=1),
     dict(nimg=2, H=20, W=20, Cin=16, N=32, KH=1, KW=1, stride=1, pad=0),
     dict(nimg=2, H=9, W=11, Cin=16, N=40, KH=2, KW=2, stride=1, pad=0),
+    # Row-window stems (Wo >= 64: a tile's <= 3 input rows bulk-copied per
+    # filter row): tiles across images, Cin 4 / 8 / 16, batch 1 (split-K).
+    dict(nimg=3, H=150, W=150, Cin=4, N=64, KH=7, KW=7, stride=2, pad=3),
+    dict(nimg=1, H=224, W=224, Cin=4, N=64, KH=7, KW=7, stride=2, pad=3),
+    dict(nimg=2, H=130, W=130, Cin=8, N=48, KH=3, KW=3, stride=1, pad=1),
+    dict(nimg=2, H=66, W=70, Cin=16, N=32, KH=2, KW=2, stride=1, pad=0),
 ]
 
 

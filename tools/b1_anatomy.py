@@ -16,7 +16,12 @@ with Executor(suite, max_batch=90, max_requests=4) as ex:
     L = len(ex.desc["nets"][0]["layers"])
     ex.profile_table(batches=sorted({1, 2, 4, 8, b}), reps=5, tune_tiles=True)
     if mode == "ncu":
-        ex.profile_span(0, 1, L, b, reps=3)
+        # run under `ncu --profile-from-start off`: only the passes below
+        import ctypes
+        rt = ctypes.CDLL("libcudart.so.12")
+        rt.cudaProfilerStart()
+        ex.profile_span(0, 1, L, b, reps=1)
+        rt.cudaProfilerStop()
     else:
         s, e, g = ex.profile_span(0, 1, L, b, reps=50)
         print(f"{suite} b={b} pdl={os.environ.get('BS_PDL', '1')}: sync {s * 1e3:.1f} eager {e * 1e3:.1f} "
