@@ -1,0 +1,4 @@
+// Drop-in shim for <batchsim/rng.hpp> (inc/rng.hpp: SplitMix64):
+// reference code compiles unchanged with -I<repo>/include and links libbs_host.so.
+#pragma once
+#include "../../paper_2304_09961_b200/csrc/host/bsb/core.hpp"

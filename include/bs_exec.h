@@ -71,6 +71,12 @@ void bs_free(char* p);
 /* suite: "small_cnn", "googlenet", "resnet50", "mobilenet_v2",
  * "resnet50_pair", "hetero3", "collab". max_requests = arena slots. */
 int bs_create(int device, const char* suite, int max_batch, int max_requests, bs_handle** out);
+/* SURVEY.md §8(b) form: also the scheduler window cap (the default "window_cap"
+ * of the sim jobs given to bs_replay / bs_serve; 0 = theirs or the
+ * reference's 500, simulator.hpp SimConfig::window_cap) and the arithmetic
+ * type ("tf32x2" / "tf32" / "bf16", as bs_set_precision; NULL = "tf32x2"). */
+int bs_create_ex(int device, const char* suite, int max_batch, int max_requests, int window_cap,
+                 const char* dtype, bs_handle** out);
 int bs_destroy(bs_handle* h);
 /* "tf32x2" (default; split-A 2xTF32 GEMMs, fp32 activations, fp32 parity),
  * "tf32" (one TF32 MMA per K step, TF32-rounded activations) or "bf16"
@@ -93,6 +99,22 @@ int bs_plan(bs_handle* h, int plan_no);
 int bs_step(bs_handle* h, int plan_no, int segment, int dnn, int layer_from, int layer_to,
             const bs_member* members, int n_members, const bs_rider* riders, int n_riders);
 int bs_step_done(bs_handle* h, const int64_t* deposited, int n);
+
+/* What bs_step_ex launched. done_event is a cudaEvent_t recorded on the
+ * handle's stream after the step (owned by the handle, re-recorded by the next
+ * bs_step_ex): the on_step_complete signal of simulator.hpp:475-516. */
+typedef struct bs_step_result {
+  int layers_run;     /* layers with a non-empty batch (step_duration's rule, :705-713) */
+  int max_batch;      /* largest per-layer batch of the step */
+  int kernels;        /* kernel launches the step issued */
+  void* done_event;   /* cudaEvent_t */
+} bs_step_result;
+/* bs_step with the §8(b) stream and result: `stream` (a cudaStream_t, or
+ * NULL) orders the step after the work already enqueued on it, and the
+ * stream waits for the step's completion (dependent work can follow on it). */
+int bs_step_ex(bs_handle* h, int plan_no, int segment, int dnn, int layer_from, int layer_to,
+               const bs_member* members, int n_members, const bs_rider* riders, int n_riders, void* stream,
+               bs_step_result* out);
 /* Copies the request's class probabilities (or logits) out and frees its slot. */
 int bs_retire(bs_handle* h, int64_t id, float* out, int n, int logits);
 int bs_drop(bs_handle* h, int64_t id);

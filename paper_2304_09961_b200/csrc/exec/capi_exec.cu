@@ -1,6 +1,7 @@
 #include <cstdio>
 #include <cstdlib>
 // C-ABI of libbs_exec.so (declared in include/bs_exec.h).
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +22,11 @@ using namespace bs200;
 
 struct bs_handle {
   std::unique_ptr<Executor> ex;
+  int window_cap = 0;              // default sim window for bs_replay / bs_serve jobs (0: job's own / 500)
+  cudaEvent_t step_done = nullptr;  // bs_step_ex completion event (owned)
+  ~bs_handle() {
+    if (step_done) cudaEventDestroy(step_done);
+  }
 };
 
 namespace {
@@ -123,6 +129,21 @@ int bs_create(int device, const char* suite, int max_batch, int max_requests, bs
   });
 }
 
+int bs_create_ex(int device, const char* suite, int max_batch, int max_requests, int window_cap, const char* dtype,
+                 bs_handle** out) {
+  return guarded([&] {
+    if (window_cap < 0) throw std::invalid_argument("bs_create_ex: window_cap < 0");
+    bs_handle* h = nullptr;
+    const int rc = bs_create(device, suite, max_batch, max_requests, &h);
+    if (rc != BS_OK) return rc;
+    std::unique_ptr<bs_handle> own(h);
+    h->window_cap = window_cap;
+    if (dtype && *dtype) h->ex->set_precision(dtype);
+    *out = own.release();
+    return static_cast<int>(BS_OK);
+  });
+}
+
 int bs_destroy(bs_handle* h) {
   return guarded([&] {
     delete h;
@@ -181,6 +202,45 @@ int bs_step(bs_handle* h, int plan_no, int segment, int dnn, int layer_from, int
   });
 }
 
+int bs_step_ex(bs_handle* h, int plan_no, int segment, int dnn, int layer_from, int layer_to, const bs_member* m,
+               int nm, const bs_rider* r, int nr, void* stream, bs_step_result* out) {
+  return guarded([&] {
+    if (!h || (nm > 0 && !m) || (nr > 0 && !r)) throw std::invalid_argument("bs_step_ex: bad argument");
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    Executor& ex = *h->ex;
+    if (!h->step_done && cudaEventCreateWithFlags(&h->step_done, cudaEventDisableTiming) != cudaSuccess)
+      throw std::runtime_error("bs_step_ex: event");
+    if (user) {  // the step follows the work already enqueued on the caller's stream
+      if (cudaEventRecord(h->step_done, user) != cudaSuccess ||
+          cudaStreamWaitEvent(ex.stream(), h->step_done, 0) != cudaSuccess)
+        throw std::runtime_error("bs_step_ex: stream order");
+    }
+    const long k0 = ex.launches();
+    const int rc = bs_step(h, plan_no, segment, dnn, layer_from, layer_to, m, nm, r, nr);
+    if (rc != BS_OK) return rc;
+    if (cudaEventRecord(h->step_done, ex.stream()) != cudaSuccess) throw std::runtime_error("bs_step_ex: event");
+    if (user && cudaStreamWaitEvent(user, h->step_done, 0) != cudaSuccess)
+      throw std::runtime_error("bs_step_ex: stream order");
+    if (out) {
+      // the batch rule of step_duration (simulator.hpp:705-713), as Executor::step applies it
+      int first = layer_from;
+      for (int i = 0; i < nm; ++i) first = std::min(first, m[i].layer);
+      out->layers_run = 0;
+      out->max_batch = 0;
+      for (int k = first; k <= layer_to; ++k) {
+        int b = 0;
+        for (int i = 0; i < nm; ++i) b += m[i].layer <= k;
+        for (int i = 0; i < nr; ++i) b += r[i].join_layer <= k && k <= r[i].leave_layer;
+        out->layers_run += b > 0;
+        out->max_batch = std::max(out->max_batch, b);
+      }
+      out->kernels = static_cast<int>(ex.launches() - k0);
+      out->done_event = h->step_done;
+    }
+    return static_cast<int>(BS_OK);
+  });
+}
+
 int bs_step_done(bs_handle* h, const int64_t* deposited, int n) {
   return guarded([&] {
     h->ex->step_done(std::vector<std::int64_t>(deposited, deposited + n));
@@ -235,9 +295,18 @@ int bs_profile_span(bs_handle* h, int dnn, int from, int to, int batch, int reps
   });
 }
 
+namespace {
+// bs_create_ex's window_cap is the default of the job's sim window.
+json with_window_cap(const bs_handle* h, json j) {
+  if (h->window_cap > 0 && j.contains("sim") && j["sim"].is_object() && !j["sim"].contains("window_cap"))
+    j["sim"]["window_cap"] = h->window_cap;
+  return j;
+}
+}  // namespace
+
 int bs_replay(bs_handle* h, const char* job_json, char** out) {
   return guarded([&] {
-    const json j = json::parse(job_json);
+    const json j = with_window_cap(h, json::parse(job_json));
     batchsim::SimJob job = batchsim::sim_job_from_json(j);
     Executor& ex = *h->ex;
     ReplayHook hook;
@@ -302,7 +371,7 @@ int bs_replay(bs_handle* h, const char* job_json, char** out) {
 
 int bs_serve(bs_handle* h, const char* job_json, char** out) {
   return guarded([&] {
-    *out = dup_str(serve_live(*h->ex, json::parse(job_json)).dump());
+    *out = dup_str(serve_live(*h->ex, with_window_cap(h, json::parse(job_json))).dump());
     return BS_OK;
   });
 }

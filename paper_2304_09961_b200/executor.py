@@ -27,6 +27,10 @@ class bs_rider(C.Structure):
                 ("leave_layer", C.c_int), ("deposit_layer", C.c_int)]
 
 
+class bs_step_result(C.Structure):
+    _fields_ = [("layers_run", C.c_int), ("max_batch", C.c_int), ("kernels", C.c_int), ("done_event", C.c_void_p)]
+
+
 def _lib():
     global _declared
     lib = exec_lib()
@@ -34,6 +38,9 @@ def _lib():
         H = C.c_void_p
         sig = {
             "bs_create": ([C.c_int, C.c_char_p, C.c_int, C.c_int, C.POINTER(H)], C.c_int),
+            "bs_create_ex": ([C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(H)], C.c_int),
+            "bs_step_ex": ([H, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(bs_member), C.c_int,
+                            C.POINTER(bs_rider), C.c_int, C.c_void_p, C.POINTER(bs_step_result)], C.c_int),
             "bs_destroy": ([H], C.c_int),
             "bs_suite_json": ([H, C.POINTER(C.c_void_p)], C.c_int),
             "bs_read_weights": ([H, FP, C.c_size_t], C.c_int),
@@ -108,9 +115,14 @@ def make_image(seed: int, index: int, H: int, W: int, C_: int, real_c: int = 3) 
 
 
 class Executor:
-    def __init__(self, suite: str, device: int = 0, max_batch: int = 90, max_requests: int = 1024):
+    def __init__(self, suite: str, device: int = 0, max_batch: int = 90, max_requests: int = 1024,
+                 window_cap: int | None = None, dtype: str | None = None):
         h = C.c_void_p()
-        _check(_lib().bs_create(device, suite.encode(), max_batch, max_requests, C.byref(h)))
+        if window_cap is None and dtype is None:
+            _check(_lib().bs_create(device, suite.encode(), max_batch, max_requests, C.byref(h)))
+        else:  # the SURVEY.md §8(b) form
+            _check(_lib().bs_create_ex(device, suite.encode(), max_batch, max_requests, window_cap or 0,
+                                       dtype.encode() if dtype else None, C.byref(h)))
         self._h = h
         self.suite_name = suite
         self.max_batch = max_batch
@@ -168,6 +180,18 @@ class Executor:
         r = (bs_rider * max(1, len(riders)))(*[bs_rider(*x) for x in riders])
         _check(_lib().bs_step(self._h, plan_no, segment, dnn, layer_from, layer_to, m, len(members), r,
                               len(riders)))
+
+    def step_ex(self, plan_no: int, segment: int, dnn: int, layer_from: int, layer_to: int,
+                members: list[tuple[int, int]], riders: list[tuple] = (), stream: int | None = None) -> dict:
+        """bs_step_ex: ordered after / awaited by `stream` (a cudaStream_t as an
+        int, or None); returns the step result (done_event = cudaEvent_t)."""
+        m = (bs_member * max(1, len(members)))(*[bs_member(i, l) for i, l in members])
+        r = (bs_rider * max(1, len(riders)))(*[bs_rider(*x) for x in riders])
+        res = bs_step_result()
+        _check(_lib().bs_step_ex(self._h, plan_no, segment, dnn, layer_from, layer_to, m, len(members), r,
+                                 len(riders), C.c_void_p(stream) if stream else None, C.byref(res)))
+        return {"layers_run": res.layers_run, "max_batch": res.max_batch, "kernels": res.kernels,
+                "done_event": res.done_event}
 
     def step_done(self, deposited: list[int]):
         arr = (C.c_int64 * max(1, len(deposited)))(*deposited)

@@ -429,3 +429,31 @@ def test_live_serve_collab_config5():
         w = ex.weights()
         orcs = [NetOracle(ex.desc, k, w) for k in range(len(names))]
         assert _check_live_outputs(ex, r, 9, pool, orcs) >= 3
+
+
+@pytest.mark.gpu
+def test_create_ex_and_step_ex_boundary():
+    """SURVEY.md §8(b) forms: bs_create_ex (window cap, dtype) and bs_step_ex
+    ordered on a caller stream, with the step result and its completion event."""
+    import ctypes
+    import torch
+    from paper_2304_09961_b200.executor import Executor, make_image
+    from oracle.forward import NetOracle, assert_request_matches
+    with Executor("googlenet", max_batch=8, max_requests=8, window_cap=200, dtype="tf32x2") as ex:
+        orc = NetOracle(ex.desc, 0, ex.weights())
+        n = ex.desc["nets"][0]
+        imgs = [make_image(5, i, n["in_H"], n["in_W"], n["in_C"]) for i in range(3)]
+        for i, img in enumerate(imgs):
+            ex.admit(i + 1, 0, img)
+        ex.plan(1)
+        s = torch.cuda.Stream()
+        # requests 1-2 through layers 1-10, then all three (request 3 catches up) to 22
+        r1 = ex.step_ex(1, 0, 0, 1, 10, [(1, 1), (2, 1)], stream=s.cuda_stream)
+        assert r1["layers_run"] == 10 and r1["max_batch"] == 2 and r1["kernels"] > 10 and r1["done_event"]
+        r2 = ex.step_ex(1, 1, 0, 11, 22, [(1, 11), (2, 11), (3, 1)], stream=s.cuda_stream)
+        assert r2["layers_run"] == 22 and r2["max_batch"] == 3
+        s.synchronize()  # the caller's stream waited for the step
+        rt = ctypes.CDLL("libcudart.so.12")
+        assert rt.cudaEventQuery(ctypes.c_void_p(r2["done_event"])) == 0
+        for i, img in enumerate(imgs):
+            assert_request_matches(ex.retire(i + 1, 1000), orc.probs(orc.forward(img)), 1e-3)
