@@ -89,10 +89,14 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   // One TMA descriptor per conv/FC weight matrix (weights never move).
   wmaps_.resize(suite_.nets.size());
   wmaps_wide_.resize(suite_.nets.size());
+  wmaps_mid_.resize(suite_.nets.size());
+  wmaps_mid160_.resize(suite_.nets.size());
   for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
     const NetDef& net = suite_.nets[n];
     wmaps_[n].resize(net.ops.size());
     wmaps_wide_[n].resize(net.ops.size());
+    wmaps_mid_[n].resize(net.ops.size());
+    wmaps_mid160_[n].resize(net.ops.size());
     for (std::size_t i = 0; i < net.ops.size(); ++i) {
       const OpDef& op = net.ops[i];
       if (op.kind != OpKind::conv) continue;
@@ -101,6 +105,12 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
       if (op.out.C > 128 &&
           !encode_weight_map(&wmaps_wide_[n][i], d_weights_ + op.w_off, op.out.C, op.Kpad, 256))
         throw std::runtime_error("cuTensorMapEncodeTiled (wide) failed for " + op.name);
+      if (op.out.C > 128 &&
+          !encode_weight_map(&wmaps_mid_[n][i], d_weights_ + op.w_off, op.out.C, op.Kpad, 192))
+        throw std::runtime_error("cuTensorMapEncodeTiled (mid) failed for " + op.name);
+      if (op.out.C > 128 &&
+          !encode_weight_map(&wmaps_mid160_[n][i], d_weights_ + op.w_off, op.out.C, op.Kpad, 160))
+        throw std::runtime_error("cuTensorMapEncodeTiled (mid160) failed for " + op.name);
     }
   }
   // Tap-row mode for the stems (default; BS_CONV_TAPROW=0 disables): one K
@@ -338,6 +348,8 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
     const std::size_t oi = static_cast<std::size_t>(&op - net.ops.data());
     p.wmap = bf ? wmaps_bf_[ni][oi] : wmaps_[ni][oi];
     if (op.out.C > 128) conv_add_wide_map(p, bf ? wmaps_wide_bf_[ni][oi] : wmaps_wide_[ni][oi]);
+    if (op.out.C > 128 && !bf) conv_add_mid_map(p, wmaps_mid_[ni][oi]);
+    if (op.out.C > 128 && !bf) conv_add_mid160_map(p, wmaps_mid160_[ni][oi]);
   }
   p.nimg = batch;
   p.H = ti.H;
@@ -873,6 +885,8 @@ std::string Executor::tune_tiles(const std::vector<int>& batches, int reps) {
             std::vector<ConvChoice> cands{{0, 0}};
             for (signed char ks : {1, 2, 4, 8}) cands.push_back({2, ks});
             if (op.out.C > 128) cands.push_back({1, 1});
+            if (op.out.C > 128 && prec_ != 2) cands.push_back({3, 1});
+            if (op.out.C > 128 && prec_ != 2) cands.push_back({4, 1});
             tune_op_ = oi;
             ConvChoice best{};
             double best_ms = 1e30;

@@ -145,7 +145,7 @@ class Executor {
 
  private:
   struct ConvChoice {
-    signed char wide = 0;  // 0 launcher rule, 1 128 x 256, 2 128-wide
+    signed char wide = 0;  // 0 launcher rule, 1 128 x 256, 2 128-wide, 3 128 x 192, 4 128 x 160
     signed char ks = 0;    // 0 launcher cost model, else forced K split
   };
   int tuned_index(int batch) const;                              // nearest tuned batch, -1 if none
@@ -207,6 +207,8 @@ class Executor {
   std::vector<int> pool_n_;
   std::vector<std::vector<CUtensorMap>> wmaps_;  // [net][op] weight tensor maps
   std::vector<std::vector<CUtensorMap>> wmaps_wide_;  // [net][op] 256-row boxes (N > 128)
+  std::vector<std::vector<CUtensorMap>> wmaps_mid_;   // [net][op] 192-row boxes (N > 128)
+  std::vector<std::vector<CUtensorMap>> wmaps_mid160_;  // [net][op] 160-row boxes (N > 128)
   struct TapRowMap {
     bool ok = false;
     CUtensorMap wmap{};

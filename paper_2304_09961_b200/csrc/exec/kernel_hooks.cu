@@ -29,6 +29,8 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
   float** ptrs = nullptr;
   std::uint16_t* dbf = nullptr;  // bf16 weight copy (d->split == 2)
   CUtensorMap wide;              // 256-row weight box (the launcher keeps a pointer)
+  CUtensorMap mid;               // 192-row weight box
+  CUtensorMap mid160;            // 160-row weight box
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   int rc = BS_OK;
 #define CK(x)                                           \
@@ -75,6 +77,16 @@ extern "C" int bs_kernel_conv(const bs_conv_desc* d, int nimg, const float* in_h
         goto done;
       }
       conv_add_wide_map(p, wide);
+      if (!encode_weight_map(&mid, dw, d->N, Kpad, 192)) {
+        rc = bs_fail(BS_ECUDA, "cuTensorMapEncodeTiled (mid) failed");
+        goto done;
+      }
+      conv_add_mid_map(p, mid);
+      if (!encode_weight_map(&mid160, dw, d->N, Kpad, 160)) {
+        rc = bs_fail(BS_ECUDA, "cuTensorMapEncodeTiled (mid160) failed");
+        goto done;
+      }
+      conv_add_mid160_map(p, mid160);
     }
     p.out_ptrs = ptrs + nimg; p.out_ldc = d->out_ldc; p.out_off = d->out_coff;
     p.res_ptrs = dres ? ptrs + 2 * nimg : nullptr; p.res_ldc = d->res_ldc; p.res_off = d->res_coff;

@@ -72,6 +72,31 @@ bool use_wide(const ConvParams& p, int sms) {
 }  // namespace
 
 void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide) { p.wmap_wide = &wide; }
+void conv_add_mid_map(ConvParams& p, const CUtensorMap& mid) { p.wmap_mid = &mid; }
+void conv_add_mid160_map(ConvParams& p, const CUtensorMap& mid160) { p.wmap_mid160 = &mid160; }
+
+namespace {
+// 128 x 192 tiles (two TMEM accumulators, 2xTF32 / TF32 only): the tuned
+// choice (wide_pref 3), else by rule when 192 divides N and 128 does not
+// (N = 192: one exact tile instead of 25% padding at 256 or 128 + 64).
+// BS_CONV_BN192=0 never, =2 always (when a 192-row map exists).
+bool use_mid(const ConvParams& p) {
+  const char* env = std::getenv("BS_CONV_BN192");  // read per launch (tests toggle it)
+  if (!p.wmap_mid || p.prec == 2 || (env && env[0] == '0')) return false;
+  if (env && env[0] == '2') return true;
+  if (p.wide_pref) return p.wide_pref == 3;
+  return p.N > 128 && p.N % 192 == 0 && p.N % 128 != 0;
+}
+// 128 x 160 tiles: tuned (wide_pref 4), else when 160 divides N and neither
+// 128 nor 192 does (N = 160, 320, 480). BS_CONV_BN160=0 never, =2 always.
+bool use_mid160(const ConvParams& p) {
+  const char* env = std::getenv("BS_CONV_BN160");
+  if (!p.wmap_mid160 || p.prec == 2 || (env && env[0] == '0')) return false;
+  if (env && env[0] == '2') return true;
+  if (p.wide_pref) return p.wide_pref == 4;
+  return p.N > 128 && p.N % 160 == 0 && p.N % 128 != 0 && p.N % 192 != 0;
+}
+}  // namespace
 
 namespace {
 // The driver entry point is resolved through the runtime, so the library has
@@ -178,6 +203,10 @@ cudaError_t launch_prec(const ConvParams& p, const ConvParams& p2, int bn, int g
   if (bn == 32) return launch_bn<32, PREC, false>(p, p2, grid, stream);
   if (bn == 64) return launch_bn<64, PREC, false>(p, p2, grid, stream);
   if (bn == 128) return launch_bn<128, PREC, false>(p, p2, grid, stream);
+  if constexpr (PREC != 2) {
+    if (bn == 192) return launch_bn<192, PREC, false>(p, p2, grid, stream);
+    if (bn == 160) return launch_bn<160, PREC, false>(p, p2, grid, stream);
+  }
   return launch_bn<256, PREC, false>(p, p2, grid, stream);
 }
 
@@ -197,7 +226,13 @@ cudaError_t launch_conv_tc(ConvParams p, cudaStream_t stream) {
   if (p.tap_rows && (!conv_tap_rows_eligible(p.Cin, p.KW) || p.Kpad != p.KH * conv_tc::kBK))
     return cudaErrorInvalidValue;
   p.m_tiles = (p.nimg * p.Ho * p.Wo + conv_tc::kBM - 1) / conv_tc::kBM;
-  if (use_wide(p, sms)) {
+  if (use_mid(p)) {
+    bn = 192;
+    p.wmap = *p.wmap_mid;
+  } else if (use_mid160(p)) {
+    bn = 160;
+    p.wmap = *p.wmap_mid160;
+  } else if (use_wide(p, sms)) {
     bn = 256;
     p.wmap = *p.wmap_wide;
   }
@@ -241,7 +276,7 @@ cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream
     if (choose_ksplits(tiles, q->Kpad / conv_tc::kBK, sm_count()) > 1) return cudaErrorNotSupported;
     ConvParams t = *q;
     t.m_tiles = (q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM;
-    if (use_wide(t, sm_count())) return cudaErrorNotSupported;  // 128 x 256 tiles beat the group
+    if (use_wide(t, sm_count()) || use_mid(t) || use_mid160(t)) return cudaErrorNotSupported;  // 128 x 256 / 192 tiles beat the group
   }
   ks = force ? std::max(1, std::min({ks, 8, a.Kpad / conv_tc::kBK, b.Kpad / conv_tc::kBK})) : 1;
   for (ConvParams* q : {&a, &b}) {

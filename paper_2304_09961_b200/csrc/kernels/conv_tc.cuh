@@ -85,7 +85,8 @@ struct ConvParams {
   // both and the small one stops paying a launch + pipeline fill of its own.
   int group_units;
   // Tile-width preference from the executor's profile-time autotune:
-  // 0 = launcher rule, 1 = 128 x 256 tiles (needs has_wide), 2 = 128-wide.
+  // 0 = launcher rule, 1 = 128 x 256 tiles (needs wmap_wide), 2 = 128-wide,
+  // 3 = 128 x 192 tiles (needs wmap_mid), 4 = 128 x 160 (needs wmap_mid160).
   int wide_pref;
   // K-split override from the same autotune: 0 = launcher cost model, else
   // the split count (clamped to the K tiles and the cluster limit of 8).
@@ -94,6 +95,13 @@ struct ConvParams {
   // Host side only (the launcher swaps it into wmap for 128 x 256 tiles):
   // weights map with a 256-row box (N > 128), owned by the caller.
   const CUtensorMap* wmap_wide;
+  // Host side only: weights map with a 192-row box (N > 128) for 128 x 192
+  // tiles -- N = 192 in one tile, or 384 / 576 in exact tiles, with two TMEM
+  // accumulators (the 256-wide tile has one); owned by the caller.
+  const CUtensorMap* wmap_mid;
+  // Host side only: the same with a 160-row box (128 x 160 tiles: N = 320 in
+  // two exact tiles instead of 128 + 128 + 64), owned by the caller.
+  const CUtensorMap* wmap_mid160;
 };
 
 
@@ -1055,8 +1063,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
 
 }  // namespace conv_tc
 
-// Narrow N tile for N output channels (the launcher may widen to 256, see
-// conv_add_wide_map).
+// Narrow N tile for N output channels (the launcher may widen to 192 / 256,
+// see conv_add_wide_map / conv_add_mid_map).
 int conv_tile_n(int N);
 
 // Tap-row mode eligibility (Cin 4 / 8 / 16 and at most one padded tap per
@@ -1071,6 +1079,10 @@ bool encode_weight_map_bf16(CUtensorMap* map, const void* w_bf16, int N, int Kpa
 // Offers the launcher 128 x 256 tiles (weights map with box_n = 256; the map
 // must outlive the launch call).
 void conv_add_wide_map(ConvParams& p, const CUtensorMap& wide);
+// Offers the launcher 128 x 192 / 128 x 160 tiles (weights maps with
+// box_n = 192 / 160).
+void conv_add_mid_map(ConvParams& p, const CUtensorMap& mid);
+void conv_add_mid160_map(ConvParams& p, const CUtensorMap& mid160);
 // Grouped launch of two independent convs (no data flow between them; same
 // precision; cp.async gather path, no split-K): one persistent grid walks the
 // units of a, then of b, with a common tile width.

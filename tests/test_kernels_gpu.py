@@ -208,3 +208,30 @@ def test_conv_wide_tiles(case, split, monkeypatch):
     """128 x 256 tiles (single TMEM accumulator), forced with BS_CONV_BN256=2."""
     monkeypatch.setenv("BS_CONV_BN256", "2")
     assert run_conv(**case, split=split) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [
+    dict(nimg=3, H=28, W=28, Cin=64, N=192, KH=3, KW=3, stride=1, pad=1),
+    dict(nimg=2, H=14, W=14, Cin=96, N=208, KH=3, KW=3, stride=1, pad=1),
+    dict(nimg=5, H=7, W=7, Cin=256, N=384, KH=1, KW=1, stride=1, pad=0),
+    dict(nimg=1, H=14, W=14, Cin=128, N=192, KH=3, KW=3, stride=1, pad=1),  # small M: split-K clusters
+], ids=lambda c: f"b{c['nimg']}_N{c['N']}_k{c['KH']}")
+@pytest.mark.parametrize("split", [0, 1])
+def test_conv_192_wide_tiles(case, split, monkeypatch):
+    # 128 x 192 tiles (two TMEM accumulators), forced
+    monkeypatch.setenv("BS_CONV_BN192", "2")
+    assert run_conv(**case, split=split, residual=True, relu=1) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [
+    dict(nimg=2, H=14, W=14, Cin=160, N=320, KH=3, KW=3, stride=1, pad=1),
+    dict(nimg=3, H=7, W=7, Cin=64, N=160, KH=1, KW=1, stride=1, pad=0),
+    dict(nimg=1, H=14, W=14, Cin=96, N=480, KH=3, KW=3, stride=1, pad=1),  # split-K clusters
+], ids=lambda c: f"b{c['nimg']}_N{c['N']}_k{c['KH']}")
+def test_conv_160_wide_tiles(case, monkeypatch):
+    # 128 x 160 tiles (two TMEM accumulators), forced
+    monkeypatch.setenv("BS_CONV_BN160", "2")
+    monkeypatch.setenv("BS_CONV_BN192", "0")
+    assert run_conv(**case, split=1, residual=True, relu=1) < TOL
