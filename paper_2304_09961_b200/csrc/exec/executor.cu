@@ -76,6 +76,14 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
     ck(cudaMallocHost(&c.host, chunk_cap_ * sizeof(float*)), "pinned table");
     ck(cudaMalloc(&c.dev, chunk_cap_ * sizeof(float*)), "device table");
     ck(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&c.uploaded, cudaEventDisableTiming), "event");
+  }
+  {
+    const char* ts = std::getenv("BS_TABLE_STREAM");
+    table_stream_ = !(ts && ts[0] == '0');
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    ck(cudaStreamCreateWithPriority(&table_, cudaStreamNonBlocking, hi), "table stream");
   }
   // Scratch blobs for the profiler (max_batch of them) + an L2 flush buffer.
   scratch_ = ride_arena_ + static_cast<std::size_t>(n_ride_) * slot_floats_;
@@ -238,6 +246,7 @@ Executor::~Executor() {
     cudaFreeHost(c.host);
     cudaFree(c.dev);
     cudaEventDestroy(c.done);
+    cudaEventDestroy(c.uploaded);
   }
   if (copy_) cudaStreamSynchronize(copy_);
   for (cudaEvent_t e : ready_ring_) cudaEventDestroy(e);
@@ -255,6 +264,7 @@ Executor::~Executor() {
   cudaStreamDestroy(stream_);
   cudaStreamDestroy(side_);
   cudaStreamDestroy(copy_);
+  cudaStreamDestroy(table_);
 }
 
 cudaEvent_t Executor::next_ready_event() {
@@ -778,7 +788,16 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
       if (rr.join <= k && k <= rr.leave) host[j++] = rr.buf;
     runs.push_back({k, d, b});
   }
-  ck(cudaMemcpyAsync(c.dev, c.host, chunk_used_ * sizeof(float*), cudaMemcpyHostToDevice, stream_), "table H2D");
+  if (table_stream_) {
+    // the chunk's previous step has finished (host-synchronised above), so
+    // the upload may overwrite it at once; the serving stream waits for it
+    ck(cudaMemcpyAsync(c.dev, c.host, chunk_used_ * sizeof(float*), cudaMemcpyHostToDevice, table_), "table H2D");
+    ck(cudaEventRecord(c.uploaded, table_), "table uploaded");
+    ck(cudaStreamWaitEvent(stream_, c.uploaded, 0), "wait table");
+    pdl::suppress_next();
+  } else {
+    ck(cudaMemcpyAsync(c.dev, c.host, chunk_used_ * sizeof(float*), cudaMemcpyHostToDevice, stream_), "table H2D");
+  }
   for (const LayerRun& lr : runs) {
     for (const RideRun& rr : rides)
       if (rr.join == lr.k)

@@ -190,9 +190,16 @@ class Executor {
   struct TableChunk {
     float** host = nullptr;
     float** dev = nullptr;
-    cudaEvent_t done = nullptr;
+    cudaEvent_t done = nullptr;      // recorded on the serving stream after the step
+    cudaEvent_t uploaded = nullptr;  // recorded on table_ after the H2D upload
     bool in_use = false;
   };
+  // Step pointer tables are uploaded on their own top-priority stream, ahead
+  // of the serving stream, which only waits on the upload's event: the H2D
+  // copy's latency leaves the serving stream's critical path
+  // (BS_TABLE_STREAM=0: inline copy on the serving stream).
+  cudaStream_t table_ = nullptr;
+  bool table_stream_ = true;
   std::vector<TableChunk> chunks_;
   std::size_t chunk_cap_ = 0;
   std::size_t chunk_ = 0;
