@@ -171,10 +171,14 @@ void Executor::plan_groups() {
   plans_.assign(suite_.nets.size(), {});
   gmaps_.assign(suite_.nets.size(), {});
   gmap_ok_.assign(suite_.nets.size(), {});
+  gmaps192_.assign(suite_.nets.size(), {});
+  gmap192_ok_.assign(suite_.nets.size(), {});
   for (std::size_t n = 0; n < suite_.nets.size(); ++n) {
     const NetDef& net = suite_.nets[n];
     gmaps_[n].resize(net.ops.size());
     gmap_ok_[n].assign(net.ops.size(), 0);
+    gmaps192_[n].resize(net.ops.size());
+    gmap192_ok_[n].assign(net.ops.size(), 0);
     auto overlap = [&](const TRef& x, const TRef& y) {
       if (x.t < 0 || y.t < 0) return false;
       if (x.t == y.t) return x.coff < y.coff + y.C && y.coff < x.coff + x.C;
@@ -232,6 +236,16 @@ void Executor::plan_groups() {
             throw std::runtime_error("group weight map failed for " + op.name);
           gmap_ok_[n][static_cast<std::size_t>(k)] = 1;
         }
+        // 192-row maps of both convs when the wider one spans more than one
+        // 128-wide tile (the launcher may run the pair as 128 x 192 tiles)
+        if (std::max(x.out.C, y.out.C) > 128)
+          for (int k : {it.a, it.b}) {
+            const OpDef& op = net.ops[static_cast<std::size_t>(k)];
+            if (!encode_weight_map(&gmaps192_[n][static_cast<std::size_t>(k)], d_weights_ + op.w_off, op.out.C,
+                                   op.Kpad, 192))
+              throw std::runtime_error("group weight map (192) failed for " + op.name);
+            gmap192_ok_[n][static_cast<std::size_t>(k)] = 1;
+          }
       }
       plans_[n].push_back(std::move(items));
     }
@@ -439,6 +453,10 @@ void Executor::launch_group(const NetDef& net, int layer, int item, const OpDef&
   const std::size_t ia = static_cast<std::size_t>(&a - net.ops.data()), ib = static_cast<std::size_t>(&b - net.ops.data());
   if (gmap_ok_[ni][ia]) pa.wmap = prec_ == 2 ? gmaps_bf_[ni][ia] : gmaps_[ni][ia];
   if (gmap_ok_[ni][ib]) pb.wmap = prec_ == 2 ? gmaps_bf_[ni][ib] : gmaps_[ni][ib];
+  // group maps at 192 rows (launch_conv_tc_group's 128 x 192 option)
+  pa.wmap_mid = prec_ != 2 && gmap192_ok_[ni][ia] ? &gmaps192_[ni][ia] : nullptr;
+  pb.wmap_mid = prec_ != 2 && gmap192_ok_[ni][ib] ? &gmaps192_[ni][ib] : nullptr;
+  pa.wmap_mid160 = pb.wmap_mid160 = nullptr;
   LaunchStat st{};
   const bool sample = stats_on_ && (++stats_seen_ % stats_every_ == 0) && ev_next_ + 2 <= event_pool_.size();
   if (sample) {

@@ -230,6 +230,8 @@ class Executor {
   };
   std::vector<std::vector<std::vector<LayerItem>>> plans_;  // [net][layer - 1]
   std::vector<std::vector<CUtensorMap>> gmaps_;              // [net][op] weights at the group's tile width
+  std::vector<std::vector<CUtensorMap>> gmaps192_;           // [net][op] 192-row boxes for 128 x 192 grouped launches
+  std::vector<std::vector<char>> gmap192_ok_;
   std::vector<std::vector<char>> gmap_ok_;
   float* d_tap_weights_ = nullptr;                // (kh, kw < 32 / Cin, ci) copies of the stem weights
   long total_slots_ = 0;

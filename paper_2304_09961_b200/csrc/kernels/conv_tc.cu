@@ -195,7 +195,9 @@ int choose_ksplits(int tiles, int KT, int sms) {
 
 template <int PREC>
 cudaError_t launch_prec(const ConvParams& p, const ConvParams& p2, int bn, int grid, cudaStream_t stream) {
-  if (p.group_units) {  // grouped launches use tile widths <= 128
+  if (p.group_units) {  // grouped launches use tile widths <= 128, or 192
+    if constexpr (PREC != 2)
+      if (bn == 192) return launch_bn<192, PREC, true>(p, p2, grid, stream);
     if (bn == 32) return launch_bn<32, PREC, true>(p, p2, grid, stream);
     if (bn == 64) return launch_bn<64, PREC, true>(p, p2, grid, stream);
     return launch_bn<128, PREC, true>(p, p2, grid, stream);
@@ -266,7 +268,23 @@ cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream
     if (q->Cin % 4 != 0 || q->Kpad % conv_tc::kBK != 0 || q->Kpad < q->K || q->nimg <= 0 || q->tap_rows ||
         q->prec != a.prec)
       return cudaErrorInvalidValue;
-  const int bn = std::max(conv_tile_n(a.N), conv_tile_n(b.N));
+  int bn = std::max(conv_tile_n(a.N), conv_tile_n(b.N));
+  // 128 x 192 tiles for the pair (group maps at 192 rows in wmap_mid) when
+  // they cut the wider conv's N tiles (N = 176 / 192 / 288 / 320 / 384 ...);
+  // BS_CONV_G192=0 disables.
+  const char* e192 = std::getenv("BS_CONV_G192");
+  // Only when the pair still fills the GPU with the wider tiles (at small
+  // batches fewer, wider tiles cost parallelism: GoogLeNet b=8 +4%).
+  const int big = std::max(a.N, b.N);
+  const int big_m = (a.N >= b.N ? a.nimg * a.Ho * a.Wo : b.nimg * b.Ho * b.Wo);
+  const bool g192 = !(e192 && e192[0] == '0') && a.prec != 2 && a.wmap_mid && b.wmap_mid && big > 128 &&
+                    (big + 191) / 192 < (big + 127) / 128 &&
+                    ((big_m + conv_tc::kBM - 1) / conv_tc::kBM) * ((big + 191) / 192) >= sm_count();
+  if (g192) {
+    bn = 192;
+    a.wmap = *a.wmap_mid;
+    b.wmap = *b.wmap_mid;
+  }
   // Unforced, a group is unsplit: decline (the caller launches the two convs
   // separately) when either conv would be split on its own.
   for (const ConvParams* q : {&a, &b}) {
@@ -276,7 +294,8 @@ cudaError_t launch_conv_tc_group(ConvParams a, ConvParams b, cudaStream_t stream
     if (choose_ksplits(tiles, q->Kpad / conv_tc::kBK, sm_count()) > 1) return cudaErrorNotSupported;
     ConvParams t = *q;
     t.m_tiles = (q->nimg * q->Ho * q->Wo + conv_tc::kBM - 1) / conv_tc::kBM;
-    if (use_wide(t, sm_count()) || use_mid(t) || use_mid160(t)) return cudaErrorNotSupported;  // 128 x 256 / 192 tiles beat the group
+    // 128 x 256 / 160 / 192 tiles beat the group (192: unless the group itself runs 192-wide)
+    if (use_wide(t, sm_count()) || (use_mid(t) && !g192) || use_mid160(t)) return cudaErrorNotSupported;
   }
   ks = force ? std::max(1, std::min({ks, 8, a.Kpad / conv_tc::kBK, b.Kpad / conv_tc::kBK})) : 1;
   for (ConvParams* q : {&a, &b}) {
