@@ -575,6 +575,8 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
     s.ready = next_ready_event();
     ck(cudaEventRecord(s.ready, copy_), "ready rec");
     s.pending_ready = true;
+    s.ready_seq = ++ready_seq_;
+    s.ready_stream = 0;
   } else {
     // Collaborative mode: the client's layer prefix, emulated on a side
     // stream so it stays off the server's critical path.
@@ -601,6 +603,8 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
     s.ready = next_ready_event();
     ck(cudaEventRecord(s.ready, side_), "ready rec");
     s.pending_ready = true;
+    s.ready_seq = ++ready_seq_;
+    s.ready_stream = 1;
   }
   slot_of_.emplace(id, s);
 }
@@ -626,7 +630,23 @@ void Executor::admit_rgb(std::int64_t id, int dnn, const float* rgb) {
   s.ready = next_ready_event();
   ck(cudaEventRecord(s.ready, copy_), "ready rec");
   s.pending_ready = true;
+  s.ready_seq = ++ready_seq_;
+  s.ready_stream = 0;
   slot_of_.emplace(id, s);
+}
+
+void Executor::wait_ready(const std::vector<Slot*>& pending) {
+  Slot* latest[2] = {nullptr, nullptr};
+  for (Slot* s : pending) {
+    Slot*& l = latest[s->ready_stream];
+    if (!l || s->ready_seq > l->ready_seq) l = s;
+  }
+  for (Slot* l : latest)
+    if (l) {
+      ck(cudaStreamWaitEvent(stream_, l->ready, 0), "wait ready");
+      pdl::suppress_next();
+    }
+  for (Slot* s : pending) s->pending_ready = false;
 }
 
 void Executor::wait_slot_free(int index, cudaStream_t st) {
@@ -721,15 +741,12 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
                     const std::vector<batchsim::Rider>& riders) {
   if (plan_no != ride_plan_) new_plan(plan_no);
   const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
-  // Members whose prefix (collaborative entry) is still running.
+  // Members whose input copy / client prefix may still be running.
+  std::vector<Slot*> pending;
   for (const auto& [id, layer] : members) {
     auto it = slot_of_.find(id);
     if (it == slot_of_.end()) throw std::logic_error("step member not admitted: " + std::to_string(id));
-    if (it->second.pending_ready) {
-      ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
-      pdl::suppress_next();
-      it->second.pending_ready = false;
-    }
+    if (it->second.pending_ready) pending.push_back(&it->second);
   }
   // Members sorted by current layer: the batch at layer k is a prefix.
   std::vector<std::pair<int, float*>> mem;
@@ -749,11 +766,7 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     if (r.join_layer > to || r.leave_layer < from) continue;
     auto it = slot_of_.find(r.id);
     if (it == slot_of_.end()) continue;  // dropped meanwhile
-    if (it->second.pending_ready) {
-      ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
-      pdl::suppress_next();
-      it->second.pending_ready = false;
-    }
+    if (it->second.pending_ready) pending.push_back(&it->second);
     auto rb = ride_of_.find(r.id);
     float* buf;
     if (rb == ride_of_.end()) {
@@ -767,6 +780,8 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     }
     rides.push_back({r.join_layer, r.leave_layer, buf, it->second.blob});
   }
+
+  wait_ready(pending);
 
   // One pointer chunk per step.
   chunk_ = (chunk_ + 1) % chunks_.size();

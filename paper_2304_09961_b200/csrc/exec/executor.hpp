@@ -123,6 +123,11 @@ class Executor {
     float* blob = nullptr;
     cudaEvent_t ready = nullptr;  // input copy / client prefix finished (ring-owned)
     bool pending_ready = false;
+    // order of its ready event on its admission stream (0 copy_, 1 side_):
+    // events on one stream complete in order, so a step waits only on the
+    // latest pending one per stream
+    long ready_seq = 0;
+    int ready_stream = 0;
   };
   float* slot_ptr(int index) const { return arena_ + static_cast<std::size_t>(index) * slot_floats_; }
   float** table_alloc(std::size_t n, float*** host_view);
@@ -171,6 +176,10 @@ class Executor {
   std::size_t staging_floats_ = 0;
   int staging_n_ = 0, staging_next_ = 0;
   cudaEvent_t next_ready_event();
+  long ready_seq_ = 0;
+  // One stream wait per admission stream for the pending members / riders
+  // of a step (the latest-admitted one's ready event covers the rest).
+  void wait_ready(const std::vector<Slot*>& pending);
   float* d_weights_ = nullptr;
   float* arena_ = nullptr;
   std::size_t slot_floats_ = 0;
