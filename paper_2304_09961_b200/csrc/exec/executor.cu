@@ -63,9 +63,9 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   // A freed slot may still be read by work queued on the serving stream (the
   // retiring request's D2H copy of its probabilities); its next admission
   // writes it from the copy or side stream, so it first waits on this event.
-  slot_free_ev_.resize(static_cast<std::size_t>(n_slots_));
-  slot_free_pending_.assign(static_cast<std::size_t>(n_slots_), 0);
-  for (auto& e : slot_free_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "slot event");
+  slot_free_.assign(static_cast<std::size_t>(n_slots_), FreeMark{});
+  free_ring_.resize(4096);
+  for (auto& e : free_ring_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "slot event");
   ride_arena_ = arena_ + static_cast<std::size_t>(n_slots_) * slot_floats_;
   for (int i = n_ride_ - 1; i >= 0; --i) ride_free_.push_back(i);
   int max_layers = 1;
@@ -264,7 +264,7 @@ Executor::~Executor() {
   }
   if (copy_) cudaStreamSynchronize(copy_);
   for (cudaEvent_t e : ready_ring_) cudaEventDestroy(e);
-  for (cudaEvent_t e : slot_free_ev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : free_ring_) cudaEventDestroy(e);
   cudaFree(staging_);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (float* p : pool_) cudaFree(p);
@@ -649,12 +649,24 @@ void Executor::wait_ready(const std::vector<Slot*>& pending) {
   for (Slot* s : pending) s->pending_ready = false;
 }
 
+Executor::FreeMark Executor::record_free() {
+  // A re-recorded ring event (after 4096 frees) only waits for a later point.
+  FreeMark m{free_ring_[free_next_], ++free_seq_};
+  free_next_ = (free_next_ + 1) % free_ring_.size();
+  ck(cudaEventRecord(m.ev, stream_), "slot free rec");
+  return m;
+}
+
 void Executor::wait_slot_free(int index, cudaStream_t st) {
-  const std::size_t i = static_cast<std::size_t>(index);
-  if (!slot_free_pending_[i]) return;
-  ck(cudaStreamWaitEvent(st, slot_free_ev_[i], 0), "wait slot free");
-  pdl::suppress_next();
-  slot_free_pending_[i] = 0;
+  FreeMark& f = slot_free_[static_cast<std::size_t>(index)];
+  if (!f.seq) return;
+  long& waited = waited_free_[st == side_ ? 1 : 0];
+  if (f.seq > waited) {
+    ck(cudaStreamWaitEvent(st, f.ev, 0), "wait slot free");
+    pdl::suppress_next();
+    waited = f.seq;  // every free up to this one is covered on st
+  }
+  f.seq = 0;
 }
 
 const float* Executor::blob(std::int64_t id) const {
@@ -684,7 +696,7 @@ void Executor::retire_async(std::int64_t id, float* out, int n) {
   ck(cudaMemcpyAsync(out, it->second.blob + t.off, static_cast<std::size_t>(cnt) * sizeof(float),
                      cudaMemcpyDeviceToHost, stream_),
      "retire copy");
-  drop(id);  // the slot's next admission waits for this copy (slot_free_ev_)
+  drop(id);  // the slot's next admission waits for this copy (slot_free_)
 }
 
 void Executor::retire_many_async(const std::vector<std::int64_t>& ids, const std::vector<float*>& outs, int n) {
@@ -704,10 +716,23 @@ void Executor::retire_many_async(const std::vector<std::int64_t>& ids, const std
     }
     ck(launch_gather_out(g, stream_), "retire gather");
   }
-  for (std::int64_t id : ids) drop(id);  // slot reuse waits for the gather (slot_free_ev_)
+  // One release mark after the gather for all of them (slot reuse waits for it).
+  if (ids.empty()) return;
+  for (std::int64_t id : ids) {
+    auto it = slot_of_.find(id);
+    if (it != slot_of_.end() && it->second.pending_ready) {
+      ck(cudaStreamWaitEvent(stream_, it->second.ready, 0), "wait ready");
+      pdl::suppress_next();
+      it->second.pending_ready = false;
+    }
+  }
+  const FreeMark m = record_free();
+  for (std::int64_t id : ids) release_slot(id, &m);
 }
 
-void Executor::drop(std::int64_t id) {
+void Executor::drop(std::int64_t id) { release_slot(id, nullptr); }
+
+void Executor::release_slot(std::int64_t id, const FreeMark* shared) {
   auto it = slot_of_.find(id);
   if (it == slot_of_.end()) return;
   if (it->second.pending_ready) {
@@ -716,8 +741,7 @@ void Executor::drop(std::int64_t id) {
     pdl::suppress_next();
   }
   const std::size_t idx = static_cast<std::size_t>(it->second.index);
-  ck(cudaEventRecord(slot_free_ev_[idx], stream_), "slot free rec");
-  slot_free_pending_[idx] = 1;
+  slot_free_[idx] = shared ? *shared : record_free();
   free_.push_back(it->second.index);
   slot_of_.erase(it);
   auto r = ride_of_.find(id);

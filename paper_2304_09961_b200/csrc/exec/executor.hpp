@@ -185,8 +185,21 @@ class Executor {
   std::size_t slot_floats_ = 0;
   int n_slots_ = 0;
   std::vector<int> free_;
-  std::vector<cudaEvent_t> slot_free_ev_;  // recorded on stream_ when a slot is freed
-  std::vector<char> slot_free_pending_;
+  // Slot release marks: a ring event recorded on stream_ when slots are
+  // freed (one per batched retire, shared by its slots) and its sequence
+  // number. Frees are ordered on stream_, so an admission stream that has
+  // waited on free #S needs no wait for any slot freed at or before S.
+  struct FreeMark {
+    cudaEvent_t ev = nullptr;
+    long seq = 0;  // 0: nothing pending
+  };
+  std::vector<FreeMark> slot_free_;
+  std::vector<cudaEvent_t> free_ring_;
+  std::size_t free_next_ = 0;
+  long free_seq_ = 0;
+  long waited_free_[2] = {0, 0};  // copy_, side_
+  FreeMark record_free();
+  void release_slot(std::int64_t id, const FreeMark* shared);
   void wait_slot_free(int index, cudaStream_t st);
   std::unordered_map<std::int64_t, Slot> slot_of_;
   // ride buffers: rider id -> ride slot index (valid for the current plan)
