@@ -378,7 +378,8 @@ def run_ours(a, ws, rank, local) -> dict | None:
         "vs_baseline": None,
         "dtype": {"tf32x2": "f32 (tf32x2 tcgen05 MMA, fp32 accumulate)", "tf32": "f32 (tf32 MMA)",
                   "bf16": "bf16 (bf16 tcgen05 MMA operands, fp32 accumulate, fp32 activations)"}[a.precision],
-        "data": "synthetic images (SplitMix64 N(0,1)), deterministic random-init weights",
+        "data": "synthetic 8-bit RGB images (SplitMix64 N(0,1) draws quantised to 1/32 steps; e2e ships the "
+                "bytes, the device path holds their exact fp32 values), deterministic calibrated random-init weights",
         "on_time_ratio": round(tot_on / tot_gen, 4) if tot_gen else None,
         "config": {
             "workload": cfg["workload"],

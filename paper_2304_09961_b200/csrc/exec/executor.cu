@@ -52,7 +52,7 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
     for (const NetDef& n : suite_.nets) mx = std::max<std::size_t>(mx, static_cast<std::size_t>(n.in_H) * n.in_W * 3);
     staging_floats_ = (mx + 63) / 64 * 64;
     staging_n_ = 64;
-    ck(cudaMalloc(&staging_, staging_floats_ * staging_n_ * sizeof(float)), "rgb staging");
+    ck(cudaMalloc(&staging_, staging_floats_ * staging_n_), "rgb staging");
   }
   // One slot space: [request slots | ride buffers | profiler scratch], so a
   // single TMA tensor map per layer input addresses every blob by slot index.
@@ -609,7 +609,7 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
   slot_of_.emplace(id, s);
 }
 
-void Executor::admit_rgb(std::int64_t id, int dnn, const float* rgb) {
+void Executor::admit_rgb(std::int64_t id, int dnn, const std::uint8_t* rgb) {
   if (slot_of_.count(id)) throw std::logic_error("request admitted twice: " + std::to_string(id));
   if (free_.empty()) throw std::runtime_error("activation arena full");
   const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
@@ -621,10 +621,9 @@ void Executor::admit_rgb(std::int64_t id, int dnn, const float* rgb) {
   s.dnn = dnn;
   s.blob = slot_ptr(s.index);
   const int hw = in.H * in.W;
-  float* stage = staging_ + static_cast<std::size_t>(staging_next_) * staging_floats_;
+  std::uint8_t* stage = staging_ + static_cast<std::size_t>(staging_next_) * staging_floats_;
   staging_next_ = (staging_next_ + 1) % staging_n_;  // ring reuse is ordered on copy_
-  ck(cudaMemcpyAsync(stage, rgb, static_cast<std::size_t>(hw) * 3 * sizeof(float), cudaMemcpyHostToDevice, copy_),
-     "admit rgb H2D");
+  ck(cudaMemcpyAsync(stage, rgb, static_cast<std::size_t>(hw) * 3, cudaMemcpyHostToDevice, copy_), "admit rgb H2D");
   wait_slot_free(s.index, copy_);
   ck(launch_expand_rgb(stage, s.blob + in.off, hw, copy_), "expand rgb");
   s.ready = next_ready_event();

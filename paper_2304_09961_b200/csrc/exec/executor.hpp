@@ -54,10 +54,11 @@ class Executor {
   // ---- request lifecycle
   // image: NHWC [in_H][in_W][in_C] floats, on host (copied H2D) or device.
   void admit(std::int64_t id, int dnn, int entry_layer, const float* image, bool on_device);
-  // Packed RGB [H][W][3] in pinned host memory: H2D on the copy stream into a
-  // staging ring, expanded to the padded input tensor on the device; the
-  // request's first step waits for it (copies overlap compute).
-  void admit_rgb(std::int64_t id, int dnn, const float* rgb_pinned);
+  // Packed 8-bit RGB [H][W][3] in pinned host memory (csrc/exec/image.hpp
+  // encoding): H2D on the copy stream into a staging ring, expanded to the
+  // padded fp32 input tensor on the device; the request's first step waits
+  // for it (copies overlap compute).
+  void admit_rgb(std::int64_t id, int dnn, const std::uint8_t* rgb_pinned);
   void retire(std::int64_t id, float* probs_host, int n, bool logits = false);  // synchronous copy
   void retire_async(std::int64_t id, float* probs_pinned, int n);               // stream-ordered copy + free
   // Batched retire: one copy-out kernel for all ids (pinned, device-mapped
@@ -172,8 +173,8 @@ class Executor {
   cudaStream_t copy_ = nullptr;  // admissions (H2D / D2D input copies)
   std::vector<cudaEvent_t> ready_ring_;
   std::size_t ready_next_ = 0;
-  float* staging_ = nullptr;     // RGB staging ring
-  std::size_t staging_floats_ = 0;
+  std::uint8_t* staging_ = nullptr;  // 8-bit RGB staging ring
+  std::size_t staging_floats_ = 0;      // bytes per staging slot
   int staging_n_ = 0, staging_next_ = 0;
   cudaEvent_t next_ready_event();
   long ready_seq_ = 0;

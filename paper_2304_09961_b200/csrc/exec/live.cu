@@ -60,25 +60,22 @@ json serve_live(Executor& ex, const json& j) {
 
   // Inputs: device-resident pool (kernel-level runs) or pinned host images
   // copied H2D at admission (end-to-end runs).
-  std::vector<float*> host_pool(suite.nets.size(), nullptr);
-  std::vector<std::size_t> img_floats(suite.nets.size(), 0);
+  std::vector<std::uint8_t*> host_pool(suite.nets.size(), nullptr);
+  std::vector<std::size_t> img_floats(suite.nets.size(), 0);  // bytes per packed 8-bit RGB image
   for (std::size_t d = 0; d < dnn_map.size(); ++d) {
     const int net = dnn_map[d];
     const NetDef& nd = suite.nets[static_cast<std::size_t>(net)];
-    // e2e runs ship packed RGB (3 channels) from pinned host memory.
+    // e2e runs ship the images as decoded 8-bit RGB from pinned host memory
+    // (csrc/exec/image.hpp: the same pixels the device-resident pool holds).
     img_floats[static_cast<std::size_t>(net)] = static_cast<std::size_t>(nd.in_H) * nd.in_W * 3;
     if (h2d) {
       if (!host_pool[static_cast<std::size_t>(net)]) {
-        float* p = nullptr;
-        if (cudaMallocHost(&p, img_floats[static_cast<std::size_t>(net)] * pool * sizeof(float)) != cudaSuccess)
+        std::uint8_t* p = nullptr;
+        if (cudaMallocHost(&p, img_floats[static_cast<std::size_t>(net)] * pool) != cudaSuccess)
           throw std::runtime_error("pinned image pool");
-        std::vector<float> padded(static_cast<std::size_t>(nd.in_H) * nd.in_W * nd.in_C);
-        for (int i = 0; i < pool; ++i) {
-          synth_image(image_seed, static_cast<std::uint64_t>(i), nd.in_H, nd.in_W, nd.in_C, 3, padded.data());
-          float* dst = p + img_floats[static_cast<std::size_t>(net)] * static_cast<std::size_t>(i);
-          for (long px = 0; px < static_cast<long>(nd.in_H) * nd.in_W; ++px)
-            for (int ch = 0; ch < 3; ++ch) dst[px * 3 + ch] = padded[static_cast<std::size_t>(px) * nd.in_C + ch];
-        }
+        for (int i = 0; i < pool; ++i)
+          synth_image_bytes(image_seed, static_cast<std::uint64_t>(i), nd.in_H, nd.in_W, 3,
+                            p + img_floats[static_cast<std::size_t>(net)] * static_cast<std::size_t>(i));
         host_pool[static_cast<std::size_t>(net)] = p;
       }
     } else if (ex.pool_size(net) < pool) {
@@ -212,7 +209,7 @@ json serve_live(Executor& ex, const json& j) {
       const int img = static_cast<int>(i % static_cast<std::size_t>(pool));
       if (h2d && adm[ai].entry_layer == 1) {
         ex.admit_rgb(id, net, host_pool[static_cast<std::size_t>(net)] + img_floats[static_cast<std::size_t>(net)] * img);
-        h2d_bytes += static_cast<long>(img_floats[static_cast<std::size_t>(net)] * sizeof(float));
+        h2d_bytes += static_cast<long>(img_floats[static_cast<std::size_t>(net)]);
       } else {
         ex.admit(id, net, adm[ai].entry_layer, ex.pool_image(net, img), true);
       }
@@ -396,7 +393,7 @@ json serve_live(Executor& ex, const json& j) {
       dumped[std::to_string(id)] = std::vector<float>(results + (id - 1) * classes, results + id * classes);
   }
   cudaFreeHost(results);
-  for (float* p : host_pool)
+  for (std::uint8_t* p : host_pool)
     if (p) cudaFreeHost(p);
   const SummaryMetrics m = summarize(outs);
   const double span_s = (last_completion - first_arrival) / 1000.0;

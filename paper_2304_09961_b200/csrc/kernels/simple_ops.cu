@@ -463,11 +463,13 @@ __global__ void gather_out_kernel(const GatherParams p) {
   for (int j = threadIdx.x; j < p.cnt; j += blockDim.x) dst[j] = src[j];
 }
 
-__global__ void expand_rgb_kernel(const float* __restrict__ rgb, float* __restrict__ dst, int hw) {
+__global__ void expand_rgb_kernel(const unsigned char* __restrict__ rgb, float* __restrict__ dst, int hw) {
   pdl::launch_dependents();
   pdl::wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < hw; i += gridDim.x * blockDim.x) {
-    const float r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
+    const float r = (static_cast<int>(rgb[3 * i]) - 128) * (1.0f / 32.0f);
+    const float g = (static_cast<int>(rgb[3 * i + 1]) - 128) * (1.0f / 32.0f);
+    const float b = (static_cast<int>(rgb[3 * i + 2]) - 128) * (1.0f / 32.0f);
     reinterpret_cast<float4*>(dst)[i] = make_float4(r, g, b, 0.f);
   }
 }
@@ -487,7 +489,7 @@ cudaError_t launch_to_bf16(const float* src, std::uint16_t* dst, std::size_t n, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand_rgb(const float* rgb, float* dst, int hw, cudaStream_t s) {
+cudaError_t launch_expand_rgb(const unsigned char* rgb, float* dst, int hw, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   pdl::suppress_next();  // admission copy stream: after an H2D copy / event wait
   e = pdl::launch(expand_rgb_kernel, dim3(grid_for(hw)), dim3(kThreads), 0, s, rgb, dst, hw);

@@ -53,7 +53,9 @@ struct SoftmaxParams {
 
 // Packed RGB [HW][3] -> padded NHWC [HW][4] (4th channel zero), the request's
 // input tensor. Lets clients ship 3 channels over PCIe.
-cudaError_t launch_expand_rgb(const float* rgb, float* dst, int hw, cudaStream_t s);
+// 8-bit packed RGB [hw][3] -> padded fp32 [hw][4] with value (b - 128) / 32
+// (the synthetic images' pixel encoding, csrc/exec/image.hpp).
+cudaError_t launch_expand_rgb(const unsigned char* rgb, float* dst, int hw, cudaStream_t s);
 cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s);
 cudaError_t launch_avgpool(const AvgPoolParams& p, cudaStream_t s);
 cudaError_t launch_dwconv(const DwParams& p, cudaStream_t s);
