@@ -1035,6 +1035,30 @@ double Executor::profile_layer(int dnn, int layer, int batch, int reps, bool flu
   return ms[ms.size() / 2];
 }
 
+double Executor::profile_pass_total(int dnn, int batch, int reps) {
+  if (batch < 1 || batch > max_batch_) throw std::invalid_argument("profile batch out of range");
+  const int L = suite_.nets[static_cast<std::size_t>(dnn)].num_layers();
+  std::vector<cudaEvent_t> ev(static_cast<std::size_t>(reps) + 1);
+  for (auto& e : ev) ck(cudaEventCreate(&e), "ev");
+  for (int w = 0; w < 2; ++w)
+    for (int k = 1; k <= L; ++k) run_layer(dnn, k, scratch_ptrs_, batch);
+  ck(cudaEventRecord(ev[0], stream_), "ev");
+  for (int r = 0; r < reps; ++r) {
+    for (int k = 1; k <= L; ++k) run_layer(dnn, k, scratch_ptrs_, batch);
+    ck(cudaEventRecord(ev[static_cast<std::size_t>(r) + 1], stream_), "ev");
+  }
+  ck(cudaStreamSynchronize(stream_), "pass sync");
+  std::vector<double> v(static_cast<std::size_t>(reps));
+  for (int r = 0; r < reps; ++r) {
+    float t = 0;
+    ck(cudaEventElapsedTime(&t, ev[static_cast<std::size_t>(r)], ev[static_cast<std::size_t>(r) + 1]), "elapsed");
+    v[static_cast<std::size_t>(r)] = t;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  std::sort(v.begin(), v.end());
+  return v[v.size() / 2];
+}
+
 std::vector<double> Executor::profile_pass(int dnn, int batch, int reps) {
   if (batch < 1 || batch > max_batch_) throw std::invalid_argument("profile batch out of range");
   const int L = suite_.nets[static_cast<std::size_t>(dnn)].num_layers();

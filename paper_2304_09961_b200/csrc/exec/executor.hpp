@@ -90,6 +90,9 @@ class Executor {
   // -- the cost a layer has in a multi-layer serving step, without the
   // launch latency and idle gaps a synchronised single-layer timing adds.
   std::vector<double> profile_pass(int dnn, int batch, int reps);
+  // Median time of one whole-network pass at batch b, passes back to back
+  // with events only between passes (ms).
+  double profile_pass_total(int dnn, int batch, int reps);
   // Layers [from, to] at one batch on scratch blobs, per pass (ms):
   // out[0] = synchronised per pass (launch latency included), out[1] = reps
   // passes queued back to back, out[2] = one CUDA graph of the pass replayed.

@@ -462,9 +462,29 @@ json measure_profile(Executor& ex, const json& opts) {
   if (timing != "pass" && timing != "layer") throw std::invalid_argument("timing: pass | layer");
   // pass timings of every net at every batch: [net][batch index][layer - 1]
   std::vector<std::vector<std::vector<double>>> pass_ms(s.nets.size());
+  // The events between layers break the programmatic-dependent-launch
+  // overlap a multi-layer step has, so the per-layer medians sum above what
+  // the same layers cost back to back. With scale_to_pass (default; env
+  // BS_TABLE_SCALE=0 disables) each (net, batch) column is scaled so that it
+  // sums to the median whole-pass time measured without inner events: the
+  // layers' relative costs come from the events, the total from the chain.
+  const char* sc_env = std::getenv("BS_TABLE_SCALE");
+  const bool scale = opts.value("scale_to_pass", true) && !(sc_env && sc_env[0] == '0');
+  json scales = json::array();
   if (timing == "pass")
     for (std::size_t i = 0; i < s.nets.size(); ++i)
-      for (int b : batches) pass_ms[i].push_back(ex.profile_pass(static_cast<int>(i), b, reps));
+      for (int b : batches) {
+        std::vector<double> col = ex.profile_pass(static_cast<int>(i), b, reps);
+        if (scale) {
+          double sum = 0;
+          for (double v : col) sum += v;
+          const double whole = ex.profile_pass_total(static_cast<int>(i), b, reps);
+          const double f = sum > 0 ? whole / sum : 1.0;
+          for (double& v : col) v *= f;
+          scales.push_back(json::array({s.nets[i].name, b, f}));
+        }
+        pass_ms[i].push_back(std::move(col));
+      }
   json comps = json::array();
   for (std::size_t c = 0; c < s.components.size(); ++c) {
     // measure a component inside the first DNN that contains it
@@ -503,6 +523,7 @@ json measure_profile(Executor& ex, const json& opts) {
   json prof = {{"max_batch", ex.max_batch()}, {"components", comps}, {"dnns", dnns}};
   if (!tuned.is_null()) prof["tile_tune"] = tuned;  // [op, batch, choice, layer ms] (extra key; opt-in)
   prof["timing"] = timing;                          // extra key (ignored by the profile parsers)
+  if (!scales.empty()) prof["pass_scale"] = scales;  // [net, batch, whole pass / sum of layers]
   return prof;
 }
 
