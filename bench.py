@@ -150,7 +150,7 @@ CONFIGS = {
         "workload": "config 2: GoogLeNet 224x224 single DNN, Poisson arrivals, Our-Tardy (on-time objective), "
                     "partial batching at layer granularity, B=90, 1 server per GPU"},
     3: {"suite": "resnet50_pair", "max_batch": 90, "process": "pareto", "scheduler": "ours-time",
-        "granularity": "group", "shared_batching": True, "pdl": False,
+        "granularity": "group", "shared_batching": True,
         "workload": "config 3: two DNNs sharing a ResNet-50 backbone (heads 1000 / 365 classes), shared-layer "
                     "merge batching with riders, Pareto arrivals (alpha 1.25), G=5, B=90"},
     4: {"suite": "hetero3", "max_batch": 90, "process": "poisson", "scheduler": "ours-time",
@@ -158,7 +158,7 @@ CONFIGS = {
         "workload": "config 4: GoogLeNet + ResNet-50 + MobileNetV2 (no shared layers), equal Poisson mix, "
                     "multi-DNN permutation DP, G=5, B=90, request streams sharded over GPUs"},
     5: {"suite": "collab", "max_batch": 90, "process": "pareto", "scheduler": "ours-tardy",
-        "granularity": "group", "offload": "partial", "clients": 1024, "deadline_t1_factor": 12.5, "pdl": False,
+        "granularity": "group", "offload": "partial", "clients": 1024, "deadline_t1_factor": 12.5,
         "workload": "config 5: collaborative partial offload (GoogLeNet + ResNet-50, Jetson Nano client "
                     "profile, LTE uplink trace x10, 1024 clients, request -> client (id - 1) % clients); the "
                     "client side replayed by the reference-semantics simulator, the server suffixes served "
@@ -173,10 +173,10 @@ def run_ours(a, ws, rank, local) -> dict | None:
     cfg = CONFIGS[a.config]
     pk = peaks()
     mb = cfg["max_batch"]
-    # Programmatic dependent launch is on by default; the Pareto configs run
-    # without it (pdl.cuh / DESIGN.md §4: their schedulers pick smaller steps
-    # on the faster small-batch table and serve less on time). An explicit
-    # BS_PDL in the environment wins. Read once, before the first launch.
+    # Programmatic dependent launch is on by default (a config may opt out
+    # with "pdl": False; none does since the latency tables are scaled to the
+    # whole-pass time, pdl.cuh). An explicit BS_PDL in the environment wins.
+    # Read once, before the first launch.
     if not cfg.get("pdl", True):
         os.environ.setdefault("BS_PDL", "0")
     pdl_on = os.environ.get("BS_PDL", "1") != "0"

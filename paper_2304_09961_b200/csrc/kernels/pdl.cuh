@@ -18,14 +18,15 @@
 //     kernel k+2 transitively sees kernel k.
 // Outside a PDL launch both instructions are no-ops.
 //
-// On by default (BS_PDL=0 disables). Measured on B200 (profiles/r02/pdl/):
-// whole-network passes GoogLeNet b=1 360 -> 252 us, ResNet-50 b=1 765 -> 557
-// us, GoogLeNet b=8 509 -> 412 us, b=90 unchanged; config 2 serves the same
-// (the latency table's T1 drops 0.42 -> 0.37 ms). The two Pareto configs (3,
-// 5) serve less on time with it: their schedulers plan on the faster
-// small-batch table and pick smaller steps (config 3 at 4000 req/s: mean
-// step 5.7 vs 8.2 requests), which lowers throughput under bursts; bench.py
-// runs those two with BS_PDL=0 and says so in the line.
+// On by default (BS_PDL=0 disables). Measured on B200 (profiles/r02/pdl/,
+// profiles/r02/anatomy/): whole-network passes GoogLeNet b=1 360 -> 252 us,
+// ResNet-50 b=1 765 -> 557 us, GoogLeNet b=8 509 -> 412 us, b=90 unchanged.
+// The per-layer latency tables are scaled to the measured whole-pass time
+// (live.cu measure_profile): layer timings with events between the layers
+// break this overlap, and with unscaled tables the Pareto configs 3 / 5
+// served less on time with PDL (their schedulers planned on step costs the
+// GPU no longer had); with scaled tables PDL serves more on every config
+// (config 3 5.7k -> 7.3k req/s, config 5 12.6k -> 13.9k).
 #pragma once
 
 #include <cuda_runtime.h>
