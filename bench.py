@@ -146,7 +146,7 @@ CONFIGS = {
         "workload": "config 1: SmallCNN 32x32 single DNN, Constant arrivals, completion-time DP (Ours-Time), "
                     "request granularity, B=10"},
     2: {"suite": "googlenet", "max_batch": 90, "process": "poisson", "scheduler": "ours-tardy",
-        "granularity": "layer", "depth": 3,
+        "granularity": "layer",
         "workload": "config 2: GoogLeNet 224x224 single DNN, Poisson arrivals, Our-Tardy (on-time objective), "
                     "partial batching at layer granularity, B=90, 1 server per GPU"},
     3: {"suite": "resnet50_pair", "max_batch": 90, "process": "pareto", "scheduler": "ours-time",
@@ -205,10 +205,11 @@ def run_ours(a, ws, rank, local) -> dict | None:
     factor = cfg.get("deadline_t1_factor", 6.25)
     deadline = a.deadline_ms if a.deadline_ms else round(factor * (t1_table or t1), 3)
     sim = sim_config(cfg, mb)
-    # steps in flight in the live loop: 3 on config 2 (measured +5% capacity over 2,
-    # profiles/r02/depth/); the multi-DNN configs 3 / 4 served less with 3 (decisions
-    # taken a step further ahead of the deadlines), so they keep 2
-    base = dict(collab_inputs(cfg), profile=prof, sim=sim, image_pool=64, pipeline_depth=cfg.get("depth", 2))
+    depth = int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 3)))  # env: A/B
+    # steps in flight in the live loop: 3 (measured against 2 with the pass-scaled
+    # tables: config 2 +5%, 4 +11%, 5 +6%, 1 +3%, 3 -4% within noise;
+    # profiles/r02/depth/)
+    base = dict(collab_inputs(cfg), profile=prof, sim=sim, image_pool=64, pipeline_depth=depth)
 
     def job(rate, count, seed, h2d=False, dl=None):
         """One serving run. N > 1: ONE global trace (N x the per-GPU rate and
@@ -396,7 +397,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "max_batch": mb,
             "precision": a.precision,
             "pdl": pdl_on,
-            "pipeline_depth": cfg.get("depth", 2),
+            "pipeline_depth": int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 3))),
             "latency_table": "cold L2 (flushed before every timed layer)" if a.table_flush_l2 else
                              "warm L2 (median of back-to-back repetitions)",
             "l2": "no flush: each step touches R x 4.6 MB request blobs (>> 126 MB L2) plus 26 MB of weights",
