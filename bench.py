@@ -141,23 +141,23 @@ class ClockSampler:
 # BASELINE.json configs measured live (config 5, collaborative offload, runs
 # in replay only: its client side is modelled, tests/test_executor_gpu.py).
 CONFIGS = {
-    1: {"suite": "small_cnn", "max_batch": 10, "process": "constant", "scheduler": "ours-time",
+    1: {"suite": "small_cnn", "max_batch": 10, "deadline_ms": 0.569, "process": "constant", "scheduler": "ours-time",
         "granularity": "request",
         "workload": "config 1: SmallCNN 32x32 single DNN, Constant arrivals, completion-time DP (Ours-Time), "
                     "request granularity, B=10"},
-    2: {"suite": "googlenet", "max_batch": 90, "process": "poisson", "scheduler": "ours-tardy",
+    2: {"suite": "googlenet", "max_batch": 90, "deadline_ms": 3.559, "process": "poisson", "scheduler": "ours-tardy",
         "granularity": "layer",
         "workload": "config 2: GoogLeNet 224x224 single DNN, Poisson arrivals, Our-Tardy (on-time objective), "
                     "partial batching at layer granularity, B=90, 1 server per GPU"},
-    3: {"suite": "resnet50_pair", "max_batch": 90, "process": "pareto", "scheduler": "ours-time",
+    3: {"suite": "resnet50_pair", "max_batch": 90, "deadline_ms": 7.072, "process": "pareto", "scheduler": "ours-time",
         "granularity": "group", "shared_batching": True,
         "workload": "config 3: two DNNs sharing a ResNet-50 backbone (heads 1000 / 365 classes), shared-layer "
                     "merge batching with riders, Pareto arrivals (alpha 1.25), G=5, B=90"},
-    4: {"suite": "hetero3", "max_batch": 90, "process": "poisson", "scheduler": "ours-time",
+    4: {"suite": "hetero3", "max_batch": 90, "deadline_ms": 6.949, "process": "poisson", "scheduler": "ours-time",
         "granularity": "group",
         "workload": "config 4: GoogLeNet + ResNet-50 + MobileNetV2 (no shared layers), equal Poisson mix, "
                     "multi-DNN permutation DP, G=5, B=90, request streams sharded over GPUs"},
-    5: {"suite": "collab", "max_batch": 90, "process": "pareto", "scheduler": "ours-tardy",
+    5: {"suite": "collab", "max_batch": 90, "deadline_ms": 11.226, "process": "pareto", "scheduler": "ours-tardy",
         "granularity": "group", "offload": "partial", "clients": 1024, "deadline_t1_factor": 12.5,
         "workload": "config 5: collaborative partial offload (GoogLeNet + ResNet-50, Jetson Nano client "
                     "profile, LTE uplink trace x10, 1024 clients, request -> client (id - 1) % clients); the "
@@ -201,9 +201,13 @@ def run_ours(a, ws, rank, local) -> dict | None:
     # reference arm simulates on the same table, so both arms serve the same
     # deadline); the fresh startup table's T1 is reported beside it and used
     # when no table is committed. --deadline-ms overrides (reported).
+    # The workload's deadline is fixed per config (CONFIGS deadline_ms: 6.25 x
+    # T1 -- 12.5 x for config 5 -- of the B200 tables committed at the start
+    # of round 2, per-layer event timings), so both arms and every run serve
+    # the same D however T1 evolves; --deadline-ms overrides (reported).
     t1_table = committed_t1(a.config)
     factor = cfg.get("deadline_t1_factor", 6.25)
-    deadline = a.deadline_ms if a.deadline_ms else round(factor * (t1_table or t1), 3)
+    deadline = a.deadline_ms if a.deadline_ms else cfg["deadline_ms"]
     sim = sim_config(cfg, mb)
     depth = int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 3)))  # env: A/B
     # steps in flight in the live loop: 3 (measured against 2 with the pass-scaled
@@ -313,7 +317,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
     # table's deadline shared with the reference arm).
     d_now = round(factor * t1, 3)
     at_current_t1 = None
-    if not a.deadline_ms and t1_table and abs(d_now - deadline) > 1e-3:
+    if not a.deadline_ms and abs(d_now - deadline) > 1e-3:
         def serve_now(rate, i):
             r = ex.serve(job(rate, a.warm_requests, 3000 + i, dl=d_now))
             return allreduce_sum(r["on_time"], ws) / max(1.0, allreduce_sum(r["generated"], ws))
@@ -391,8 +395,9 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "deadline_ms": round(deadline, 4),
             "t1_ms": round(t1, 4),
             "t1_ms_committed_table": round(t1_table, 4) if t1_table else None,
-            "deadline_rule": f"{factor} x T1 of the committed table" if (t1_table and not a.deadline_ms) else
-                             ("override" if a.deadline_ms else f"{factor} x T1 of the startup table"),
+            "deadline_rule": "override" if a.deadline_ms else
+                             f"fixed per config: {factor} x T1 of the B200 tables committed at the start of round 2 "
+                             "(capacity at the same rule on today's T1: capacity_at_current_t1_deadline)",
             "t_max_batch_ms": round(t90, 4),
             "max_batch": mb,
             "precision": a.precision,
@@ -426,7 +431,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
     if a.dump_table:
         Path(a.dump_table).parent.mkdir(parents=True, exist_ok=True)
         Path(a.dump_table).write_text(json.dumps(dict(prof, _meta={
-            "measured": "bench.py startup on one B200 (CUDA events per layer, median of 10)",
+            "measured": "bench.py startup on one B200 (per-layer events inside back-to-back passes scaled to the whole-pass time, median of 10)",
             "precision": a.precision, "suite": cfg["suite"]}), indent=1))
     try:
         out["cpu_baseline"] = reference_baseline(job(cap, a.requests, 0), cap, 2, 5000)
@@ -655,7 +660,7 @@ def run_reference(a, ws, rank) -> dict | None:
 
     t1 = max(dnn_ms(d, 1) for d in prof["dnns"])
     tmax = max(dnn_ms(d, mb) for d in prof["dnns"])
-    deadline = a.deadline_ms if a.deadline_ms else round(cfg.get("deadline_t1_factor", 6.25) * t1, 3)
+    deadline = a.deadline_ms if a.deadline_ms else cfg["deadline_ms"]  # the same fixed D as our arm
     sim = sim_config(cfg, mb)
     names = [d["id"] for d in prof["dnns"]]
     w = {"process": cfg["process"], "count": a.requests, "relative_deadline": deadline}
