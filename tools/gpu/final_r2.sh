@@ -4,6 +4,7 @@ for cfg in 2 1 3 4 5; do
   timeout 900 python bench.py --config $cfg > gpurun_out/final/bench_config$cfg.json 2> gpurun_out/final/bench_config$cfg.err
 done
 timeout 900 python bench.py --precision bf16 > gpurun_out/final/bench_config2_bf16.json 2> gpurun_out/final/bench_config2_bf16.err
+timeout 900 python bench.py --impl reference > gpurun_out/final/bench_reference.json 2> gpurun_out/final/bench_reference.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/final/launches_bench.csv \
   python bench.py --steps 2 --warmup 3 --cpu-forward 0 > /dev/null 2>&1
 for c in "90 56 64 192 3 1 1" "90 28 96 128 3 1 1" "90 224 4 64 7 2 3"; do
