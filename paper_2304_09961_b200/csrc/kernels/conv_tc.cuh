@@ -336,12 +336,12 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
       ptx::mbar_init(&b_full[s], 1);
     }
     for (int s = 0; s < TA; ++s) {
-      ptx::mbar_init(&ta_full[s], 128);
+      ptx::mbar_init(&ta_full[s], 4);  // one arrival per converter warp
       ptx::mbar_init(&ta_empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
-      ptx::mbar_init(&acc_empty[a], 128);
+      ptx::mbar_init(&acc_empty[a], 4);  // one arrival per epilogue warp
     }
     ptx::fence_mbar_init();
   }
@@ -418,7 +418,10 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&ta_full[sa]);
+        // one arrival per warp after the warp's stores are fenced (each
+        // barrier arrival is a shared-memory atomic on the K loop's path)
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&ta_full[sa]);
         if (p.trace && threadIdx.x == trace_tid && blockIdx.x == 0 && it < 48) p.trace[1024 + it * 5 + 3] = gtime();
       }
     }
@@ -781,7 +784,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
           if (ctr) p.trace[3300 + jj * 8 + 1] = gtime() + (v[31] & 1);
           if (jj == BN / 32 - 1) {
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&acc_empty[acc]);  // TMEM buffer free for unit j + kAcc
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&acc_empty[acc]);  // TMEM buffer free for unit j + kAcc
           }
           const int n0 = w.n_base + jj * 32;
           if (n0 >= p.N) return;  // warp-uniform
@@ -906,7 +910,8 @@ __global__ void __launch_bounds__(Cfg<BN, PREC>::kThreads, 1)
           ptx::tmem_ld_wait();
           if (jj == BN / 32 - 1) {
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&acc_empty[acc]);
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&acc_empty[acc]);
           }
 #pragma unroll
           for (int q = 0; q < 8; ++q)
