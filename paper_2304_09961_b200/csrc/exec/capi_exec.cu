@@ -72,7 +72,9 @@ struct ReplayHook : batchsim::StepHook {
     if (log) std::fprintf(stderr, "t=%.3f admit %lld net %d entry %d\n", t, static_cast<long long>(id), net, entry_layer);
     const NetDef& nd = ex->suite().nets[static_cast<std::size_t>(net)];
     if (pool && ex->pool_size(net) > 0) {
-      ex->admit(id, net, entry_layer, ex->pool_image(net, static_cast<int>((id - 1) % ex->pool_size(net))), true);
+      const float* img = ex->pool_image(net, static_cast<int>((id - 1) % ex->pool_size(net)));
+      if (entry_layer == 1) ex->admit_ref(id, net, img);
+      else ex->admit(id, net, entry_layer, img, true);
     } else {
       host_img.resize(static_cast<std::size_t>(nd.in_H) * nd.in_W * nd.in_C);
       synth_image(image_seed, static_cast<std::uint64_t>(id - 1), nd.in_H, nd.in_W, nd.in_C, 3, host_img.data());

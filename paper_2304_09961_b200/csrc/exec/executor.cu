@@ -71,6 +71,8 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
   int max_layers = 1;
   for (const NetDef& n : suite_.nets) max_layers = std::max(max_layers, n.num_layers());
   chunk_cap_ = static_cast<std::size_t>(max_layers) * static_cast<std::size_t>(max_batch_ + n_ride_) + 64;
+  ck(cudaMalloc(&stamps_, kStampCap * sizeof(unsigned long long)), "step stamps");
+  ck(cudaMemset(stamps_, 0, kStampCap * sizeof(unsigned long long)), "step stamps");
   chunks_.resize(kChunks);
   for (auto& c : chunks_) {
     ck(cudaMallocHost(&c.host, chunk_cap_ * sizeof(float*)), "pinned table");
@@ -79,8 +81,8 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
     ck(cudaEventCreateWithFlags(&c.uploaded, cudaEventDisableTiming), "event");
   }
   {
-    const char* ts = std::getenv("BS_TABLE_STREAM");
-    table_stream_ = !(ts && ts[0] == '0');
+    const char* tm = std::getenv("BS_TABLE_MODE");
+    if (tm && tm[0] >= '0' && tm[0] <= '2') table_mode_ = tm[0] - '0';
     int lo = 0, hi = 0;
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
     ck(cudaStreamCreateWithPriority(&table_, cudaStreamNonBlocking, hi), "table stream");
@@ -263,6 +265,7 @@ Executor::~Executor() {
     cudaEventDestroy(c.uploaded);
   }
   if (copy_) cudaStreamSynchronize(copy_);
+  cudaFree(stamps_);
   for (cudaEvent_t e : ready_ring_) cudaEventDestroy(e);
   for (cudaEvent_t e : free_ring_) cudaEventDestroy(e);
   cudaFree(staging_);
@@ -285,6 +288,12 @@ cudaEvent_t Executor::next_ready_event() {
   cudaEvent_t e = ready_ring_[ready_next_];
   ready_next_ = (ready_next_ + 1) % ready_ring_.size();
   return e;
+}
+
+std::vector<std::uint64_t> Executor::stamps() {
+  std::vector<std::uint64_t> v(kStampCap);
+  ck(cudaMemcpy(v.data(), stamps_, v.size() * sizeof(std::uint64_t), cudaMemcpyDeviceToHost), "stamps D2H");
+  return v;
 }
 
 void Executor::sync() {
@@ -388,7 +397,7 @@ ConvParams Executor::conv_params(const NetDef& net, const OpDef& op, float* cons
   p.K = op.KH * op.KW * op.in.C;
   p.Kpad = op.Kpad;
   p.N = op.out.C;
-  p.in_ptrs = d_ptrs;
+  p.in_ptrs = input_ptrs(net, op, d_ptrs);
   p.in_off = off(op.in);
   p.in_ldc = ldc(op.in);
   p.wgt = d_weights_ + op.w_off;
@@ -511,17 +520,17 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
     }
     case OpKind::maxpool: {
       PoolParams p{batch, ti.H, ti.W, op.in.C, op.Ho, op.Wo, op.KH, op.stride, op.pad,
-                   d_ptrs, off(op.in), ldc(op.in), d_ptrs, off(op.out), ldc(op.out)};
+                   input_ptrs(net, op, d_ptrs), off(op.in), ldc(op.in), d_ptrs, off(op.out), ldc(op.out)};
       e = launch_maxpool(p, stream_);
       break;
     }
     case OpKind::avgpool: {
-      AvgPoolParams p{batch, ti.H * ti.W, op.in.C, d_ptrs, off(op.in), ldc(op.in), d_ptrs, off(op.out), prec_ == 0 ? 1 : 0};
+      AvgPoolParams p{batch, ti.H * ti.W, op.in.C, input_ptrs(net, op, d_ptrs), off(op.in), ldc(op.in), d_ptrs, off(op.out), prec_ == 0 ? 1 : 0};
       e = launch_avgpool(p, stream_);
       break;
     }
     case OpKind::dwconv: {
-      DwParams p{batch, ti.H, ti.W, op.in.C, op.Ho, op.Wo, op.stride, d_ptrs, off(op.in), ldc(op.in),
+      DwParams p{batch, ti.H, ti.W, op.in.C, op.Ho, op.Wo, op.stride, input_ptrs(net, op, d_ptrs), off(op.in), ldc(op.in),
                  d_weights_ + op.w_off, d_weights_ + op.b_off, d_ptrs, off(op.out), ldc(op.out), op.relu,
                  prec_ == 0 ? op.round_out : 0};
       e = launch_dwconv(p, stream_);
@@ -609,6 +618,22 @@ void Executor::admit(std::int64_t id, int dnn, int entry_layer, const float* ima
   slot_of_.emplace(id, s);
 }
 
+void Executor::admit_ref(std::int64_t id, int dnn, const float* image) {
+  if (slot_of_.count(id)) throw std::logic_error("request admitted twice: " + std::to_string(id));
+  if (free_.empty()) throw std::runtime_error("activation arena full");
+  if (!image) throw std::invalid_argument("admit_ref: null image");
+  Slot s;
+  s.index = free_.back();
+  free_.pop_back();
+  s.dnn = dnn;
+  s.blob = slot_ptr(s.index);
+  s.image = image;
+  // Nothing is written now: the first layer's kernels write the blob on the
+  // serving stream, after any earlier work that read the slot.
+  slot_free_[static_cast<std::size_t>(s.index)].seq = 0;
+  slot_of_.emplace(id, s);
+}
+
 void Executor::admit_rgb(std::int64_t id, int dnn, const std::uint8_t* rgb) {
   if (slot_of_.count(id)) throw std::logic_error("request admitted twice: " + std::to_string(id));
   if (free_.empty()) throw std::runtime_error("activation arena full");
@@ -642,6 +667,9 @@ void Executor::wait_ready(const std::vector<Slot*>& pending) {
   }
   for (Slot* l : latest)
     if (l) {
+      // an input copy that has already landed needs no device-side wait (a
+      // cross-stream wait costs the next kernel its programmatic launch)
+      if (cudaEventQuery(l->ready) == cudaSuccess) continue;
       ck(cudaStreamWaitEvent(stream_, l->ready, 0), "wait ready");
       pdl::suppress_next();
     }
@@ -772,10 +800,20 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     if (it->second.pending_ready) pending.push_back(&it->second);
   }
   // Members sorted by current layer: the batch at layer k is a prefix.
-  std::vector<std::pair<int, float*>> mem;
+  struct Mem {
+    int first;
+    float* blob;
+    const float* image;  // admit_ref input (nullptr: the input tensor is in the blob)
+  };
+  std::vector<Mem> mem;
   mem.reserve(members.size());
-  for (const auto& [id, layer] : members) mem.emplace_back(layer, slot_of_.at(id).blob);
-  std::stable_sort(mem.begin(), mem.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  bool any_ref = false;
+  for (const auto& [id, layer] : members) {
+    const Slot& sl = slot_of_.at(id);
+    mem.push_back({layer, sl.blob, sl.image});
+    any_ref = any_ref || sl.image;
+  }
+  std::stable_sort(mem.begin(), mem.end(), [](const Mem& a, const Mem& b) { return a.first < b.first; });
 
   // Ride buffers for riders joining inside this step; riders that joined in
   // an earlier step of the same plan continue on their buffer.
@@ -783,6 +821,7 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     int join, leave;
     float* buf;
     float* committed;
+    const float* image;
   };
   std::vector<RideRun> rides;
   for (const batchsim::Rider& r : riders) {
@@ -801,7 +840,8 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     } else {
       buf = ride_arena_ + static_cast<std::size_t>(rb->second) * slot_floats_;
     }
-    rides.push_back({r.join_layer, r.leave_layer, buf, it->second.blob});
+    rides.push_back({r.join_layer, r.leave_layer, buf, it->second.blob, it->second.image});
+    any_ref = any_ref || it->second.image;
   }
 
   wait_ready(pending);
@@ -815,7 +855,9 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     int k;
     float** d;
     int b;
+    float** din;  // input-tensor table (admit_ref members), or nullptr
   };
+  const long in_off = net.tensors[static_cast<std::size_t>(net.input_t)].off;
   std::vector<LayerRun> runs;
   std::vector<std::pair<int, RideRun>> copies;  // (layer before which to copy, ride)
   std::size_t mi = 0;
@@ -838,13 +880,27 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
     if (b > max_batch_) throw std::logic_error("step batch exceeds the configured bound");
     float** host;
     float** d = table_alloc(static_cast<std::size_t>(b), &host);
-    for (std::size_t i = 0; i < mi; ++i) host[i] = mem[i].second;
+    for (std::size_t i = 0; i < mi; ++i) host[i] = mem[i].blob;
     int j = static_cast<int>(mi);
     for (const RideRun& rr : rides)
       if (rr.join <= k && k <= rr.leave) host[j++] = rr.buf;
-    runs.push_back({k, d, b});
+    float** din = nullptr;
+    if (any_ref && k == 1) {
+      // bases such that base + input offset = the referenced image
+      float** hin;
+      din = table_alloc(static_cast<std::size_t>(b), &hin);
+      for (std::size_t i = 0; i < mi; ++i) hin[i] = mem[i].image ? const_cast<float*>(mem[i].image) - in_off : mem[i].blob;
+      int jj = static_cast<int>(mi);
+      for (const RideRun& rr : rides)
+        if (rr.join <= k && k <= rr.leave) hin[jj++] = rr.image ? const_cast<float*>(rr.image) - in_off : rr.buf;
+    }
+    runs.push_back({k, d, b, din});
   }
-  if (table_stream_) {
+  if (table_mode_ == 2) {
+    // the chunk's previous step has finished (host-synchronised above)
+    ck(launch_table_write(c.dev, c.host, chunk_used_, stream_, stamps_, ++step_seq_, kStampCap), "table write");
+    launches_ += static_cast<long>((chunk_used_ + kTableWriteMax - 1) / kTableWriteMax);
+  } else if (table_mode_ == 1) {
     // the chunk's previous step has finished (host-synchronised above), so
     // the upload may overwrite it at once; the serving stream waits for it
     ck(cudaMemcpyAsync(c.dev, c.host, chunk_used_ * sizeof(float*), cudaMemcpyHostToDevice, table_), "table H2D");
@@ -859,7 +915,9 @@ void Executor::step(int plan_no, int segment, int dnn, int from, int to,
       if (rr.join == lr.k)
         ck(cudaMemcpyAsync(rr.buf, rr.committed, slot_floats_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_),
            "ride copy");
+    in_override_ = lr.din;
     run_layer(dnn, lr.k, lr.d, lr.b);
+    in_override_ = nullptr;
   }
   ck(cudaEventRecord(c.done, stream_), "chunk done");
   c.in_use = true;
@@ -1091,6 +1149,59 @@ std::vector<double> Executor::profile_pass(int dnn, int batch, int reps) {
   return out;
 }
 
+std::vector<double> Executor::profile_steps(int dnn, int batch, int reps) {
+  if (batch < 1 || batch > max_batch_) throw std::invalid_argument("profile batch out of range");
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
+  const int L = net.num_layers();
+  float** tab = nullptr;
+  ck(cudaMalloc(&tab, static_cast<std::size_t>(max_batch_) * sizeof(float*)), "step table");
+  std::vector<float*> hp(static_cast<std::size_t>(batch));
+  for (int i = 0; i < batch; ++i) hp[static_cast<std::size_t>(i)] = scratch_ + static_cast<std::size_t>(i) * slot_floats_;
+  const int classes = net.num_classes;
+  float* outs = nullptr;
+  ck(cudaHostAlloc(&outs, static_cast<std::size_t>(batch) * classes * sizeof(float), cudaHostAllocMapped), "step outs");
+  const long probs_off = net.tensors[static_cast<std::size_t>(net.probs_t)].off;
+  std::vector<std::uint64_t> seq;  // table-write (step start) numbers, reps x L
+  auto pass = [&](bool keep) {
+    for (int k = 1; k <= L; ++k) {
+      ck(launch_table_write(tab, hp.data(), hp.size(), stream_, stamps_, ++step_seq_, kStampCap), "step table");
+      ++launches_;
+      if (keep) seq.push_back(step_seq_);
+      run_layer(dnn, k, tab, batch);
+      if (k == L)  // the finishing requests' results copy-out
+        for (int b0 = 0; b0 < batch; b0 += kGatherMax) {
+          GatherParams g{};
+          g.n = std::min(kGatherMax, batch - b0);
+          g.cnt = classes;
+          for (int i = 0; i < g.n; ++i) {
+            g.src[i] = hp[static_cast<std::size_t>(b0 + i)] + probs_off;
+            g.dst[i] = outs + static_cast<std::size_t>(b0 + i) * classes;
+          }
+          ck(launch_gather_out(g, stream_), "step gather");
+        }
+    }
+  };
+  pass(false);
+  pass(false);
+  for (int r = 0; r < reps; ++r) pass(true);
+  ck(launch_table_write(tab, hp.data(), hp.size(), stream_, stamps_, ++step_seq_, kStampCap), "step table");
+  sync();
+  const std::vector<std::uint64_t> st = stamps();
+  std::vector<double> out(static_cast<std::size_t>(L));
+  std::vector<double> v(static_cast<std::size_t>(reps));
+  for (int k = 0; k < L; ++k) {
+    for (int r = 0; r < reps; ++r) {
+      const std::uint64_t q = seq[static_cast<std::size_t>(r) * L + k];
+      v[static_cast<std::size_t>(r)] = static_cast<double>(st[(q + 1) % kStampCap] - st[q % kStampCap]) * 1e-6;
+    }
+    std::sort(v.begin(), v.end());
+    out[static_cast<std::size_t>(k)] = v[v.size() / 2];
+  }
+  cudaFreeHost(outs);
+  cudaFree(tab);
+  return out;
+}
+
 void Executor::profile_span(int dnn, int from, int to, int batch, int reps, double out[3]) {
   if (batch < 1 || batch > max_batch_) throw std::invalid_argument("profile batch out of range");
   cudaEvent_t a, b;
@@ -1116,10 +1227,43 @@ void Executor::profile_span(int dnn, int from, int to, int batch, int reps, doub
   }
   std::sort(v.begin(), v.end());
   out[0] = v[v.size() / 2];
+  // BS_SPAN_STEP (diagnostic bitmask) runs the back-to-back passes as the
+  // serving loop's one-layer steps: 1 a table-write kernel before each layer
+  // (the layer reads its pointers from that table), 4 an event record after
+  // it, 8 the table by H2D on the table stream + a cross-stream event wait.
+  const char* se = std::getenv("BS_SPAN_STEP");
+  const int step_bits = se ? std::atoi(se) : 0;
+  float** tab = nullptr;
+  cudaEvent_t sev = nullptr;
+  if (step_bits) {
+    ck(cudaMalloc(&tab, static_cast<std::size_t>(max_batch_) * sizeof(float*)), "span table");
+    ck(cudaEventCreateWithFlags(&sev, cudaEventDisableTiming), "ev");
+  }
+  std::vector<float*> hp(static_cast<std::size_t>(batch));
+  for (int i = 0; i < batch; ++i) hp[static_cast<std::size_t>(i)] = scratch_ + static_cast<std::size_t>(i) * slot_floats_;
+  if (step_bits & 8) std::copy(hp.begin(), hp.end(), chunks_[0].host);
+  auto step_pass = [&] {
+    for (int k = from; k <= to; ++k) {
+      if (step_bits & 1) ck(launch_table_write(tab, hp.data(), hp.size(), stream_), "span table");
+      if (step_bits & 8) {
+        ck(cudaMemcpyAsync(tab, chunks_[0].host, hp.size() * sizeof(float*), cudaMemcpyHostToDevice, table_), "span H2D");
+        ck(cudaEventRecord(chunks_[0].uploaded, table_), "ev");
+        ck(cudaStreamWaitEvent(stream_, chunks_[0].uploaded, 0), "wait");
+        pdl::suppress_next();
+      }
+      run_layer(dnn, k, (step_bits & 9) ? tab : scratch_ptrs_, batch);
+      if (step_bits & 4) ck(cudaEventRecord(sev, stream_), "ev");
+    }
+  };
   ck(cudaEventRecord(a, stream_), "ev");
-  for (int r = 0; r < reps; ++r) pass();
+  for (int r = 0; r < reps; ++r) step_bits ? step_pass() : pass();
   ck(cudaEventRecord(b, stream_), "ev");
   out[1] = elapsed() / reps;
+  if (tab) {
+    sync();
+    cudaFree(tab);
+    cudaEventDestroy(sev);
+  }
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge = nullptr;
   ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");

@@ -59,6 +59,11 @@ class Executor {
   // padded fp32 input tensor on the device; the request's first step waits
   // for it (copies overlap compute).
   void admit_rgb(std::int64_t id, int dnn, const std::uint8_t* rgb_pinned);
+  // Device-resident input (e.g. an image pool in HBM) admitted by reference:
+  // no copy into the blob and no admission event; the request's first layer
+  // reads its input tensor straight from `image` (same NHWC layout), which
+  // must stay valid until that layer has run.
+  void admit_ref(std::int64_t id, int dnn, const float* image_device);
   void retire(std::int64_t id, float* probs_host, int n, bool logits = false);  // synchronous copy
   void retire_async(std::int64_t id, float* probs_pinned, int n);               // stream-ordered copy + free
   // Batched retire: one copy-out kernel for all ids (pinned, device-mapped
@@ -76,6 +81,13 @@ class Executor {
             const std::vector<std::pair<std::int64_t, int>>& members,
             const std::vector<batchsim::Rider>& riders);
   void step_done(const std::vector<std::int64_t>& deposited);
+  // Step stamps (diagnostics, table mode 2): step number `step_seq()` of the
+  // last step; its table-write kernel stamps the global timer (ns) once
+  // every earlier kernel has completed, i.e. the previous step's end.
+  // stamps() copies the ring (valid for the last kStampCap steps).
+  static constexpr int kStampCap = 1 << 16;
+  std::uint64_t step_seq() const { return step_seq_; }
+  std::vector<std::uint64_t> stamps();
 
   // Runs layers [from, to] of `dnn` on an explicit batch of blob pointers
   // (the inner loop of step(); also used by the profiler).
@@ -90,6 +102,12 @@ class Executor {
   // -- the cost a layer has in a multi-layer serving step, without the
   // launch latency and idle gaps a synchronised single-layer timing adds.
   std::vector<double> profile_pass(int dnn, int batch, int reps);
+  // Per-layer latency of one-layer serving steps back to back (ms, median
+  // over reps): each step is the pointer-table kernel + the layer, as step()
+  // issues it, the last layer followed by the results' copy-out kernel.
+  // Timed by the table kernels' device stamps, so nothing between two steps
+  // breaks the programmatic-launch overlap a serving step has.
+  std::vector<double> profile_steps(int dnn, int batch, int reps);
   // Median time of one whole-network pass at batch b, passes back to back
   // with events only between passes (ms).
   double profile_pass_total(int dnn, int batch, int reps);
@@ -132,11 +150,18 @@ class Executor {
     // latest pending one per stream
     long ready_seq = 0;
     int ready_stream = 0;
+    const float* image = nullptr;  // admit_ref: the input tensor lives here, not in the blob
   };
   float* slot_ptr(int index) const { return arena_ + static_cast<std::size_t>(index) * slot_floats_; }
   float** table_alloc(std::size_t n, float*** host_view);
   void launch_op(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch);
   ConvParams conv_params(const NetDef& net, const OpDef& op, float* const* d_ptrs, int batch) const;
+  // Ops reading the network's input tensor take their blob bases from this
+  // table when set (step(): admit_ref members point at image - input offset).
+  float* const* in_override_ = nullptr;
+  float* const* input_ptrs(const NetDef& net, const OpDef& op, float* const* d_ptrs) const {
+    return in_override_ && op.in.t == net.input_t ? in_override_ : d_ptrs;
+  }
   // Two independent convs of one layer in one persistent launch (falls back
   // to two launches when the launcher declines: split-K or wide tiles win).
   void launch_group(const NetDef& net, int layer, int item, const OpDef& a, const OpDef& b, float* const* d_ptrs,
@@ -220,12 +245,15 @@ class Executor {
     cudaEvent_t uploaded = nullptr;  // recorded on table_ after the H2D upload
     bool in_use = false;
   };
-  // Step pointer tables are uploaded on their own top-priority stream, ahead
-  // of the serving stream, which only waits on the upload's event: the H2D
-  // copy's latency leaves the serving stream's critical path
-  // (BS_TABLE_STREAM=0: inline copy on the serving stream).
+  unsigned long long* stamps_ = nullptr;  // device, kStampCap entries
+  std::uint64_t step_seq_ = 0;
+  // How a step's pointer table reaches the device (BS_TABLE_MODE):
+  // 2 (default) a table-write kernel on the serving stream with the pointers
+  // as launch parameters (keeps the programmatic-launch chain across steps);
+  // 1 an H2D copy on its own top-priority stream, the serving stream waiting
+  // on its event; 0 an H2D copy on the serving stream.
   cudaStream_t table_ = nullptr;
-  bool table_stream_ = true;
+  int table_mode_ = 2;
   std::vector<TableChunk> chunks_;
   std::size_t chunk_cap_ = 0;
   std::size_t chunk_ = 0;

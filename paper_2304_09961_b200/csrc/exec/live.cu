@@ -1,6 +1,7 @@
 #include "live.hpp"
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <climits>
 #include <cstring>
@@ -163,6 +164,14 @@ json serve_live(Executor& ex, const json& j) {
   double host_admit_ms = 0, host_step_ms = 0;  // host time in admissions / step issue (+ bookkeeping)
   const long launches0 = ex.launches();
   std::vector<int> step_batch_hist;
+  // BS_LIVE_STEP_TIMES=1 (diagnostics, pointer-table mode 2): per step, its
+  // predicted duration and its device time from the table-write kernels'
+  // global-timer stamps (each stamps the end of all earlier work, so step k
+  // lasted stamp(k + 1) - stamp(k); no extra launch or event).
+  const char* st_env = std::getenv("BS_LIVE_STEP_TIMES");
+  const bool step_times = st_env && std::atoi(st_env) != 0;
+  std::vector<std::uint64_t> st_seq;
+  std::vector<std::array<double, 7>> st_info;  // from, to, batch, predicted ms, in flight, new members, finishing
 
   auto finish = [&](RequestId id, double t) {
     Book& b = book[static_cast<std::size_t>(id - 1)];
@@ -211,7 +220,10 @@ json serve_live(Executor& ex, const json& j) {
         ex.admit_rgb(id, net, host_pool[static_cast<std::size_t>(net)] + img_floats[static_cast<std::size_t>(net)] * img);
         h2d_bytes += static_cast<long>(img_floats[static_cast<std::size_t>(net)]);
       } else {
-        ex.admit(id, net, adm[ai].entry_layer, ex.pool_image(net, img), true);
+        if (adm[ai].entry_layer == 1)
+          ex.admit_ref(id, net, ex.pool_image(net, img));  // HBM-resident input: read in place by layer 1
+        else
+          ex.admit(id, net, adm[ai].entry_layer, ex.pool_image(net, img), true);
       }
       Request r;
       r.id = id;
@@ -257,6 +269,7 @@ json serve_live(Executor& ex, const json& j) {
       if (next_step < steps.size()) {
         const auto hs0 = Clock::now();
         const detail::ExecStep st = steps[next_step];
+        const std::uint64_t seq0 = ex.step_seq();
         const ScheduledSegment& seg = plan.segments[static_cast<std::size_t>(st.segment)];
         // pending is FIFO by (arrival, id) and live ids are assigned in
         // arrival order, so it is sorted by id: members are found by binary
@@ -328,6 +341,15 @@ json serve_live(Executor& ex, const json& j) {
         f.ev = ev_free.back();
         ev_free.pop_back();
         cudaEventRecord(f.ev, ex.stream());
+        if (step_times && ex.step_seq() > seq0) {
+          int fresh = 0;
+          for (const auto& m : members) fresh += m.second == 1;
+          st_seq.push_back(ex.step_seq());
+          st_info.push_back({static_cast<double>(st.layer_from), static_cast<double>(st.layer_to),
+                             static_cast<double>(members.size() + seg.riders.size()), st.duration,
+                             static_cast<double>(inflight.size()), static_cast<double>(fresh),
+                             static_cast<double>(f.finishing.size())});
+        }
         f.expected_end = start_est + st.duration;
         predicted_ms += st.duration;
         inflight.push_back(std::move(f));
@@ -348,6 +370,18 @@ json serve_live(Executor& ex, const json& j) {
   const double wall = ms_since(t0);
   float device_ms = 0;
   cudaEventElapsedTime(&device_ms, dev0, dev1);
+  json step_rows = json::array();
+  if (!st_seq.empty()) {
+    const std::vector<std::uint64_t> stamp = ex.stamps();
+    const auto at = [&](std::uint64_t q) { return stamp[q % Executor::kStampCap]; };
+    for (std::size_t k = 0; k + 1 < st_seq.size(); ++k) {
+      if (st_seq[k + 1] - st_seq[0] >= static_cast<std::uint64_t>(Executor::kStampCap)) break;
+      json row = json::array();
+      for (double v : st_info[k]) row.push_back(v);
+      row.push_back(static_cast<double>(at(st_seq[k + 1]) - at(st_seq[k])) * 1e-6);
+      step_rows.push_back(row);
+    }
+  }
   cudaEventDestroy(dev0);
   cudaEventDestroy(dev1);
   for (cudaEvent_t e : ev_free) cudaEventDestroy(e);
@@ -416,6 +450,7 @@ json serve_live(Executor& ex, const json& j) {
   out["device_ms"] = device_ms;  // CUDA events on the serving stream, first admission to last retire
   out["span_ms"] = last_completion - first_arrival;
   out["steps"] = n_steps;
+  if (step_times) out["step_times"] = step_rows;  // [from, to, batch, predicted, in flight, new, finishing, device ms]
   out["plans"] = n_plans;
   out["sched_ms_total"] = sched_ms;
   out["sched_ms_max"] = max_sched_ms;
@@ -454,12 +489,17 @@ json measure_profile(Executor& ex, const json& opts) {
   const bool flush = opts.value("flush_l2", false);
   json tuned = nullptr;
   if (opts.value("tune_tiles", false)) tuned = json::parse(ex.tune_tiles(batches, std::max(3, reps / 2)));
-  // "pass" (default): each layer's latency inside back-to-back passes of its
-  // network (what a multi-layer step costs); "layer": each layer alone,
-  // synchronised (adds launch latency and idle gaps per layer; the only mode
-  // with flush_l2, which needs an L2 flush before every timed layer).
-  const std::string timing = flush ? "layer" : opts.value("timing", std::string("pass"));
-  if (timing != "pass" && timing != "layer") throw std::invalid_argument("timing: pass | layer");
+  // "step" (default): each layer as a one-layer serving step inside
+  // back-to-back passes run as such steps (pointer-table kernel + layer,
+  // results copy-out after the last; device stamps, Executor::profile_steps)
+  // -- what the live loop's layer-granular steps cost; "pass": each layer's latency inside back-to-back passes with
+  // events between the layers, columns scaled to the whole-pass time
+  // (round-2 tables); "layer": each layer alone, synchronised (adds launch
+  // latency and idle gaps per layer; the only mode with flush_l2, which needs
+  // an L2 flush before every timed layer). BS_TABLE_TIMING overrides.
+  const char* tt_env = std::getenv("BS_TABLE_TIMING");
+  const std::string timing = flush ? "layer" : (tt_env && tt_env[0]) ? std::string(tt_env) : opts.value("timing", std::string("step"));
+  if (timing != "pass" && timing != "layer" && timing != "step") throw std::invalid_argument("timing: step | pass | layer");
   // pass timings of every net at every batch: [net][batch index][layer - 1]
   std::vector<std::vector<std::vector<double>>> pass_ms(s.nets.size());
   // The events between layers break the programmatic-dependent-launch
@@ -471,6 +511,9 @@ json measure_profile(Executor& ex, const json& opts) {
   const char* sc_env = std::getenv("BS_TABLE_SCALE");
   const bool scale = opts.value("scale_to_pass", true) && !(sc_env && sc_env[0] == '0');
   json scales = json::array();
+  if (timing == "step")
+    for (std::size_t i = 0; i < s.nets.size(); ++i)
+      for (int b : batches) pass_ms[i].push_back(ex.profile_steps(static_cast<int>(i), b, reps));
   if (timing == "pass")
     for (std::size_t i = 0; i < s.nets.size(); ++i)
       for (int b : batches) {
@@ -504,7 +547,7 @@ json measure_profile(Executor& ex, const json& opts) {
       json grid = json::array();
       for (std::size_t bi = 0; bi < batches.size(); ++bi) {
         const int b = batches[bi];
-        const double ms = timing == "pass" ? pass_ms[static_cast<std::size_t>(net_idx)][bi][static_cast<std::size_t>(k - 1)]
+        const double ms = timing != "layer" ? pass_ms[static_cast<std::size_t>(net_idx)][bi][static_cast<std::size_t>(k - 1)]
                                            : ex.profile_layer(net_idx, k, b, reps, flush);
         grid.push_back(json::array({b, ms}));
       }

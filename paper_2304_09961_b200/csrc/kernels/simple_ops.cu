@@ -463,6 +463,17 @@ __global__ void gather_out_kernel(const GatherParams p) {
   for (int j = threadIdx.x; j < p.cnt; j += blockDim.x) dst[j] = src[j];
 }
 
+__global__ void table_write_kernel(const __grid_constant__ TableWriteParams p) {
+  for (int i = threadIdx.x; i < p.n; i += blockDim.x) p.dst[i] = p.src[i];
+  pdl::launch_dependents();
+  pdl::wait();  // completes after the previous kernel: keeps the stream's completion order
+  if (p.stamps && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.stamps[p.seq % static_cast<unsigned long long>(p.cap)] = t;
+  }
+}
+
 __global__ void expand_rgb_kernel(const unsigned char* __restrict__ rgb, float* __restrict__ dst, int hw) {
   pdl::launch_dependents();
   pdl::wait();
@@ -553,6 +564,22 @@ cudaError_t launch_gather_out(const GatherParams& p, cudaStream_t s) {
   if (p.n <= 0) return cudaSuccess;
   if (p.n > kGatherMax) return cudaErrorInvalidValue;
   return pdl::launch(gather_out_kernel, dim3(p.n), dim3(kThreads), 0, s, p);
+}
+
+cudaError_t launch_table_write(float** dst, float* const* src, std::size_t n, cudaStream_t s,
+                               unsigned long long* stamps, unsigned long long seq, int cap) {
+  for (std::size_t b = 0; b < n; b += kTableWriteMax) {
+    TableWriteParams p;
+    p.dst = dst + b;
+    p.stamps = b == 0 ? stamps : nullptr;
+    p.seq = seq;
+    p.cap = cap;
+    p.n = static_cast<int>(std::min<std::size_t>(kTableWriteMax, n - b));
+    for (int i = 0; i < p.n; ++i) p.src[i] = src[b + static_cast<std::size_t>(i)];
+    const cudaError_t e = pdl::launch(table_write_kernel, dim3(1), dim3(128), 0, s, p);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_softmax(const SoftmaxParams& p, cudaStream_t s) {

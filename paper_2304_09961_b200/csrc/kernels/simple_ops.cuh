@@ -70,6 +70,26 @@ struct GatherParams {
   int n, cnt;
 };
 cudaError_t launch_gather_out(const GatherParams& p, cudaStream_t s);
+// A step's pointer table written by a kernel on the serving stream: the
+// pointers travel as launch parameters, so no H2D copy and no cross-stream
+// event wait sits between two steps' kernels (either one ends the
+// programmatic-launch overlap of the previous step's tail with the next
+// step's prologue). dst must not be read by work still in flight (the
+// executor's chunk ring guarantees it), since the kernel writes before it
+// waits on the previous kernel. stamps != null: once every earlier kernel
+// of the stream has completed, the global timer (ns) goes to
+// stamps[seq % cap] (diagnostics: the previous step's end, no extra launch).
+constexpr int kTableWriteMax = 480;
+struct TableWriteParams {
+  float** dst;
+  unsigned long long* stamps;
+  unsigned long long seq;
+  int cap;
+  int n;
+  float* src[kTableWriteMax];
+};
+cudaError_t launch_table_write(float** dst, float* const* src, std::size_t n, cudaStream_t s,
+                               unsigned long long* stamps = nullptr, unsigned long long seq = 0, int cap = 1);
 // dst[i] = bf16 round-to-nearest-even of src[i] (weight copies for BF16 precision).
 cudaError_t launch_to_bf16(const float* src, std::uint16_t* dst, std::size_t n, cudaStream_t s);
 

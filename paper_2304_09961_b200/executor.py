@@ -220,13 +220,16 @@ class Executor:
         return ms.value
 
     def profile_table(self, batches=(1, 2, 4, 8, 16, 32, 64, 90), reps: int = 10, flush_l2: bool = False,
-                      tune_tiles: bool = False, timing: str = "pass") -> dict:
+                      tune_tiles: bool = False, timing: str = "step") -> dict:
         """Measured h_k(b) table in the reference schema. tune_tiles: first
         autotune every conv's launch choices per batch -- K split, tile width,
         grouped vs separate conv pairs -- (kept for later launches; timings
-        returned under "tile_tune"). timing: "pass" = each layer inside
-        back-to-back network passes (default), "layer" = each layer alone,
-        synchronised. flush_l2: cold-L2 layer timings (per-layer mode)."""
+        returned under "tile_tune"). timing: "step" (default) = each layer as
+        a one-layer serving step inside back-to-back passes run as such steps
+        (device-stamped), "pass" = each layer inside back-to-back network
+        passes with events between layers, scaled to the whole-pass time,
+        "layer" = each layer alone, synchronised. flush_l2: cold-L2 layer
+        timings (per-layer mode)."""
         out = C.c_void_p()
         opts = json.dumps({"batches": list(batches), "reps": reps, "flush_l2": bool(flush_l2),
                            "tune_tiles": bool(tune_tiles), "timing": timing})
