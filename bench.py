@@ -209,10 +209,14 @@ def run_ours(a, ws, rank, local) -> dict | None:
     factor = cfg.get("deadline_t1_factor", 6.25)
     deadline = a.deadline_ms if a.deadline_ms else cfg["deadline_ms"]
     sim = sim_config(cfg, mb)
-    depth = int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 3)))  # env: A/B
-    # steps in flight in the live loop: 3 (measured against 2 with the pass-scaled
-    # tables: config 2 +5%, 4 +11%, 5 +6%, 1 +3%, 3 -4% within noise;
-    # profiles/r02/depth/)
+    depth = int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 4)))  # env: A/B
+    # steps in flight in the live loop: 4. With the pass-scaled tables 3 beat 2
+    # (config 2 +5%, 4 +11%, 5 +6%, 1 +3%, 3 -4% within noise;
+    # profiles/r02/depth/); with the serving-step chain (pointer-table kernel,
+    # reference admission) config 2 at 57k offered is on time 0.90 at 4 vs
+    # 0.83-0.87 at 3 and 0.81-0.86 at 6, 0.75-0.81 at 8 (deeper plans further
+    # ahead of the arrivals), configs 1 / 3 / 4 neutral
+    # (profiles/r02/serving_steps/depth_*.txt)
     base = dict(collab_inputs(cfg), profile=prof, sim=sim, image_pool=64, pipeline_depth=depth)
 
     def job(rate, count, seed, h2d=False, dl=None):
@@ -402,7 +406,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "max_batch": mb,
             "precision": a.precision,
             "pdl": pdl_on,
-            "pipeline_depth": int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 3))),
+            "pipeline_depth": int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 4))),
             "latency_table": "cold L2 (flushed before every timed layer)" if a.table_flush_l2 else
                              "warm L2 (median of back-to-back repetitions)",
             "l2": "no flush: each step touches R x 4.6 MB request blobs (>> 126 MB L2) plus 26 MB of weights",

@@ -171,7 +171,7 @@ json serve_live(Executor& ex, const json& j) {
   const char* st_env = std::getenv("BS_LIVE_STEP_TIMES");
   const bool step_times = st_env && std::atoi(st_env) != 0;
   std::vector<std::uint64_t> st_seq;
-  std::vector<std::array<double, 7>> st_info;  // from, to, batch, predicted ms, in flight, new members, finishing
+  std::vector<std::array<double, 8>> st_info;  // from, to, batch, predicted ms, in flight, new members, finishing, riders
 
   auto finish = [&](RequestId id, double t) {
     Book& b = book[static_cast<std::size_t>(id - 1)];
@@ -345,10 +345,12 @@ json serve_live(Executor& ex, const json& j) {
           int fresh = 0;
           for (const auto& m : members) fresh += m.second == 1;
           st_seq.push_back(ex.step_seq());
+          int riding = 0;
+          for (const Rider& rd : seg.riders) riding += rd.join_layer <= st.layer_to && rd.leave_layer >= st.layer_from;
           st_info.push_back({static_cast<double>(st.layer_from), static_cast<double>(st.layer_to),
                              static_cast<double>(members.size() + seg.riders.size()), st.duration,
                              static_cast<double>(inflight.size()), static_cast<double>(fresh),
-                             static_cast<double>(f.finishing.size())});
+                             static_cast<double>(f.finishing.size()), static_cast<double>(riding)});
         }
         f.expected_end = start_est + st.duration;
         predicted_ms += st.duration;
@@ -450,7 +452,7 @@ json serve_live(Executor& ex, const json& j) {
   out["device_ms"] = device_ms;  // CUDA events on the serving stream, first admission to last retire
   out["span_ms"] = last_completion - first_arrival;
   out["steps"] = n_steps;
-  if (step_times) out["step_times"] = step_rows;  // [from, to, batch, predicted, in flight, new, finishing, device ms]
+  if (step_times) out["step_times"] = step_rows;  // [from, to, batch, predicted, in flight, new, finishing, riders, device ms]
   out["plans"] = n_plans;
   out["sched_ms_total"] = sched_ms;
   out["sched_ms_max"] = max_sched_ms;

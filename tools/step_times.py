@@ -36,14 +36,15 @@ print(json.dumps({k: r[k] for k in ("offered_rps", "served_rps", "on_time_ratio_
 if len(sys.argv) > 3:
     json.dump({"summary": {k: v for k, v in r.items() if not isinstance(v, (list, dict))}, "rows": rows},
               open(sys.argv[3], "w"))
-# rows: from, to, batch, predicted, in flight at launch, new members, finishing, device ms
+# rows: from, to, batch, predicted, in flight at launch, new members, finishing, riders, device ms
 if not rows:
     sys.exit(0)
 tot_p = sum(x[3] for x in rows)
-tot_a = sum(x[7] for x in rows)
+tot_a = sum(x[8] for x in rows)
 print(f"steps {len(rows)} predicted {tot_p:.2f} ms device {tot_a:.2f} ms ratio {tot_a / tot_p:.3f}")
 keys = [("in flight at launch", lambda x: int(x[4])), ("layers", lambda x: int(x[1] - x[0] + 1)),
         ("has new members", lambda x: int(x[5] > 0)), ("has finishing", lambda x: int(x[6] > 0)),
+        ("riders in step", lambda x: int(x[7])),
         ("layer", lambda x: int(x[0]))]
 if os.environ.get("BY_BATCH"):
     keys.append(("batch", lambda x: int(x[2])))
@@ -53,7 +54,7 @@ for key, f in keys:
         a = agg.setdefault(f(x), [0, 0.0, 0.0])
         a[0] += 1
         a[1] += x[3]
-        a[2] += x[7]
+        a[2] += x[8]
     print(key)
     for k in sorted(agg):
         n, p, a = agg[k]
