@@ -185,7 +185,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
     # The executor first autotunes each N > 128 conv's tile width per batch
     # (kept for the run), then measures the latency table the scheduler uses.
     prof = ex.profile_table(batches=[b for b in BATCHES if b < mb] + [mb], reps=10, tune_tiles=True,
-                            flush_l2=a.table_flush_l2)
+                            flush_l2=a.table_flush_l2, timing=table_timing(cfg))
     prof.pop("tile_tune", None)
     names = [n["name"] for n in ex.desc["nets"]]
     comp = {c["id"]: c for c in prof["components"]}
@@ -239,8 +239,14 @@ def run_ours(a, ws, rank, local) -> dict | None:
     # ---- warm-up: capacity search (largest offered rate per GPU with the
     # whole job's on-time ratio >= 0.9; the same decisions on every rank)
     def serve_trial(rate, i):
-        r = ex.serve(job(rate, a.warm_requests, 1000 + i))
-        return allreduce_sum(r["on_time"], ws) / max(1.0, allreduce_sum(r["generated"], ws))
+        # three traces per probed rate: near saturation the on-time ratio of a
+        # single 3000-request trace varies by +-0.05 from seed to seed
+        on = gen = 0
+        for s in range(3):
+            r = ex.serve(job(rate, a.warm_requests, 1000 + 10 * i + s))
+            on += r["on_time"]
+            gen += r["generated"]
+        return allreduce_sum(on, ws) / max(1.0, allreduce_sum(gen, ws))
 
     cap_search, warm_runs = capacity_search(serve_trial, mb / t90 * 1000.0, a.warmup)
     # Timed runs at 97% of the largest passing rate: the on-time ratio is steep
@@ -249,7 +255,8 @@ def run_ours(a, ws, rank, local) -> dict | None:
 
     # ---- timed steps at the capacity rate. The timed region must itself meet
     # the 0.90 on-time bar (the capacity definition); if it does not, the
-    # rate is lowered by 4% and the K steps are timed again (at most six times).
+    # rate is lowered (step_down: 4% near the bar) and the K steps are timed
+    # again (at most six times).
     retimed = []
     for attempt in range(7):
         ex.stats(True, every=a.stats_every)
@@ -282,7 +289,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
             break
         retimed.append([round(cap, 1), round(ratio, 4)])
         ex.stats(False)
-        cap *= 0.96
+        cap = step_down(cap, ratio)
     clocks = clk.summary()
     # tensor peak of the arithmetic this run uses (BF16: the measured bf16 rate)
     tc_peak = pk["bf16_tflops_sustained"] if a.precision == "bf16" else pk["tf32_tflops"]
@@ -291,8 +298,8 @@ def run_ours(a, ws, rank, local) -> dict | None:
 
     # ---- e2e: same runs through the C-ABI with H2D inputs / D2H results.
     # Same metric: served req/s at a rate where the on-time ratio still meets
-    # 0.90. Starts at the device-resident capacity and steps down 4% at a time
-    # when the H2D admission path cannot hold the deadlines there.
+    # 0.90. Starts at the device-resident rate and steps down (step_down) when
+    # the H2D admission path cannot hold the deadlines there.
     e2e_cap = cap
     e2e_steps_down = []
     for attempt in range(7):
@@ -313,7 +320,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
         if e2e_ratio >= 0.90 or attempt == 6:
             break
         e2e_steps_down.append([round(e2e_cap, 1), round(e2e_ratio, 4)])
-        e2e_cap *= 0.96
+        e2e_cap = step_down(e2e_cap, e2e_ratio)
 
     # The deadline rule applied to today's executor: D = 6.25 x T1 of the
     # startup table (tighter as single-request latency improves). Capacity
@@ -408,7 +415,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "pdl": pdl_on,
             "pipeline_depth": int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 4))),
             "latency_table": "cold L2 (flushed before every timed layer)" if a.table_flush_l2 else
-                             "warm L2 (median of back-to-back repetitions)",
+                             f"warm L2, timing '{table_timing(cfg)}' (median of back-to-back repetitions)",
             "l2": "no flush: each step touches R x 4.6 MB request blobs (>> 126 MB L2) plus 26 MB of weights",
             "parallelism": f"{ws} independent servers (request streams sharded, no collectives)",
         },
@@ -517,6 +524,29 @@ def ref_runs(job: dict, runs: list[dict]) -> list[dict]:
     if r.returncode != 0:
         raise RuntimeError(f"ref_dump failed: {r.stderr[-400:]}")
     return [json.loads(x) for x in r.stdout.splitlines() if x.strip()]
+
+
+def table_timing(cfg: dict) -> str:
+    """How the startup latency table is timed (Executor.profile_table): layer
+    granularity serves one-layer steps, so each layer is timed as such a step
+    ("step"); the group / request granularities serve multi-layer steps, whose
+    layers overlap inside the launch chain as in a whole pass ("pass": layers
+    inside back-to-back passes, scaled to the pass). Measured: config 2 serves
+    more on the step table (depth 4: 57k offered on time 0.90 vs 0.83-0.87
+    earlier), config 4 on the pass table (11k offered: 1.00 vs 0.87;
+    profiles/r02/serving_steps/table_timing_*)."""
+    return cfg.get("table_timing", "step" if cfg["granularity"] == "layer" else "pass")
+
+
+def step_down(rate: float, ratio: float) -> float:
+    """Next offered rate after a timed run missed the 0.90 on-time bar: 4%
+    lower near the bar, proportionally more far below it (a run far past
+    saturation says little about where the bar is)."""
+    if ratio >= 0.8:
+        return rate * 0.96
+    if ratio >= 0.5:
+        return rate * 0.85
+    return rate * 0.7
 
 
 def capacity_search(serve, est: float, min_runs: int, max_runs: int = 14):
@@ -674,13 +704,21 @@ def run_reference(a, ws, rank) -> dict | None:
     search_runs = []
 
     def serve(rate, i):
-        r = ref_runs(job, [{"rate": rate, "seed": 1000 + i}])[0]
-        search_runs.append(r)
-        return r["on_time_ratio"]
+        # the same probe as our arm: three traces per rate
+        rs = ref_runs(job, [{"rate": rate, "seed": 1000 + 10 * i + s} for s in range(3)])
+        search_runs.extend(rs)
+        return sum(r["on_time"] for r in rs) / max(1, sum(r["generated"] for r in rs))
 
     cap_search, warm = capacity_search(serve, mb / tmax * 1000.0, a.warmup)
     cap = cap_search * 0.97
-    timed = ref_runs(job, [{"rate": cap, "seed": 5000 + k} for k in range(a.steps)])
+    retimed = []
+    for attempt in range(7):  # the same timed-region rule as our arm
+        timed = ref_runs(job, [{"rate": cap, "seed": 5000 + k} for k in range(a.steps)])
+        ratio = sum(r["on_time"] for r in timed) / max(1, sum(r["generated"] for r in timed))
+        if ratio >= 0.90 or attempt == 6:
+            break
+        retimed.append([round(cap, 1), round(ratio, 4)])
+        cap = step_down(cap, ratio)
     completed = sum(r["completed"] for r in timed)
     span = sum(r["span_ms"] for r in timed)
     wall = sum(r["wall_ms"] for r in timed)
@@ -704,6 +742,7 @@ def run_reference(a, ws, rank) -> dict | None:
                        "max_batch": mb, "table": str(table.relative_to(ROOT)),
                        "parallelism": "reference is single-threaded (1 host core)"},
             "capacity_search": [[round(r, 1), round(x, 4)] for r, x in warm],
+            "retimed_below_target": retimed,
             "host": {"run_sim_wall_ms_per_step": round(wall / a.steps, 2),
                      "per_plan_ms": round(wall / max(1, plans), 4),
                      "requests_per_host_second": round(gen / (wall / 1000.0), 1),

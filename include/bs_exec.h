@@ -95,6 +95,11 @@ int bs_make_image(uint64_t seed, uint64_t index, int H, int W, int C, int real_c
 /* ------------------------------------------------------------- requests */
 
 int bs_admit(bs_handle* h, int64_t id, int dnn, int entry_layer, const float* image_host);
+/* Same arrival (entry_layer 1) with the NHWC fp32 input already in device
+ * memory: admitted by reference -- no copy; the request's first layer reads
+ * the image in place, so it must stay valid and unchanged until that layer
+ * has run (e.g. until the request retires). */
+int bs_admit_device(bs_handle* h, int64_t id, int dnn, const float* image_device);
 int bs_plan(bs_handle* h, int plan_no);
 int bs_step(bs_handle* h, int plan_no, int segment, int dnn, int layer_from, int layer_to,
             const bs_member* members, int n_members, const bs_rider* riders, int n_riders);

@@ -184,6 +184,13 @@ int bs_set_precision(bs_handle* h, const char* mode) {
   });
 }
 
+int bs_admit_device(bs_handle* h, int64_t id, int dnn, const float* image_device) {
+  return guarded([&] {
+    h->ex->admit_ref(id, dnn, image_device);
+    return BS_OK;
+  });
+}
+
 int bs_plan(bs_handle* h, int plan_no) {
   return guarded([&] {
     h->ex->new_plan(plan_no);

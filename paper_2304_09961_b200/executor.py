@@ -45,6 +45,7 @@ def _lib():
             "bs_suite_json": ([H, C.POINTER(C.c_void_p)], C.c_int),
             "bs_read_weights": ([H, FP, C.c_size_t], C.c_int),
             "bs_admit": ([H, C.c_int64, C.c_int, C.c_int, FP], C.c_int),
+            "bs_admit_device": ([H, C.c_int64, C.c_int, C.c_void_p], C.c_int),
             "bs_plan": ([H, C.c_int], C.c_int),
             "bs_step": ([H, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(bs_member), C.c_int,
                          C.POINTER(bs_rider), C.c_int], C.c_int),
@@ -170,6 +171,12 @@ class Executor:
     def admit(self, rid: int, dnn: int, image: np.ndarray, entry_layer: int = 1):
         image = np.ascontiguousarray(image, np.float32)
         _check(_lib().bs_admit(self._h, rid, dnn, entry_layer, image.ctypes.data_as(FP)))
+
+    def admit_device(self, rid: int, dnn: int, image_ptr: int):
+        """Admit with the NHWC fp32 input already in device memory (e.g. a
+        torch CUDA tensor's data_ptr()): read in place by the first layer, so
+        it must outlive that layer."""
+        _check(_lib().bs_admit_device(self._h, rid, dnn, C.c_void_p(image_ptr)))
 
     def plan(self, plan_no: int):
         _check(_lib().bs_plan(self._h, plan_no))

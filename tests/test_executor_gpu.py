@@ -71,6 +71,31 @@ def test_googlenet_ragged_steps_match_oracle(googlenet):
         assert_request_matches(p, p_ref, TOL)
 
 
+def test_admit_device_reads_input_in_place(googlenet):
+    """bs_admit_device: inputs in HBM admitted by reference (no copy into the
+    blob), mixed in one ragged step with copied admissions -- outputs match
+    the oracle, and the referenced images are left untouched."""
+    import torch
+    ex, w = googlenet
+    orc = NetOracle(ex.desc, 0, w)
+    imgs = {i: image_for(ex, 0, i + 40) for i in (41, 42, 43, 44)}
+    dev = {i: torch.from_numpy(imgs[i].copy()).cuda() for i in (41, 43)}
+    for i, img in imgs.items():
+        if i in dev:
+            ex.admit_device(i, 0, dev[i].data_ptr())
+        else:
+            ex.admit(i, 0, img)
+    ex.plan(2)
+    ex.step(2, 0, 0, 1, 4, [(41, 1), (42, 1)])
+    ex.step(2, 1, 0, 1, 22, [(43, 1), (44, 1), (41, 5), (42, 5)])
+    for i in imgs:
+        p_ref = orc.probs(orc.forward(imgs[i]))
+        assert_request_matches(ex.retire(i, 1000), p_ref, TOL)
+    torch.cuda.synchronize()
+    for i, t in dev.items():
+        assert np.array_equal(t.cpu().numpy(), imgs[i])
+
+
 def test_googlenet_full_batch_90(googlenet):
     ex, w = googlenet
     orc = NetOracle(ex.desc, 0, w)
@@ -138,6 +163,28 @@ def test_resnet50_pair_riders_and_rewind():
         rb = ob.probs(ob.forward(ib))
         assert_request_matches(pa, ra, TOL)
         assert_request_matches(pb, rb, TOL)
+
+
+def test_riders_admitted_by_reference():
+    """A rider whose input was admitted by reference (bs_admit_device) rides
+    the shared backbone from layer 1: its ride buffer takes the input from the
+    referenced image."""
+    import torch
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("resnet50_pair", max_batch=90, max_requests=16) as ex:
+        w = ex.weights()
+        oa, ob = NetOracle(ex.desc, 0, w), NetOracle(ex.desc, 1, w)
+        ia, ib = image_for(ex, 0, 5), image_for(ex, 1, 6)
+        da, db = torch.from_numpy(ia.copy()).cuda(), torch.from_numpy(ib.copy()).cuda()
+        ex.admit_device(1, 0, da.data_ptr())
+        ex.admit_device(2, 1, db.data_ptr())
+        ex.plan(1)
+        ex.step(1, 0, 0, 1, 49, [(1, 1)], [(2, 1, 1, 49, 50)])
+        ex.step_done([2])
+        ex.step(1, 0, 0, 50, 50, [(1, 50)])
+        ex.step(1, 1, 1, 50, 51, [(2, 50)])
+        assert_request_matches(ex.retire(1, 1000), oa.probs(oa.forward(ia)), TOL)
+        assert_request_matches(ex.retire(2, 365), ob.probs(ob.forward(ib)), TOL)
 
 
 def test_mobilenet_v2_matches_oracle():
@@ -393,6 +440,28 @@ def test_live_serve_h2d_outputs_match_oracle():
         assert r["completed"] + r["dropped"] == 200 and r["h2d_bytes"] > 0
         orc = NetOracle(ex.desc, 0, ex.weights())
         assert _check_live_outputs(ex, r, 4, pool, [orc]) >= 4
+
+
+def test_live_serve_device_resident_outputs_match_oracle():
+    """The bench's `value` path: HBM-resident pool images admitted by
+    reference (layer 1 reads each image in place, no admission copy), at a
+    load high enough for full batches -- served probabilities match the
+    oracle, for more requests than there are pool images (each image is read
+    by many requests, never written)."""
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("googlenet", max_batch=90, max_requests=512) as ex:
+        prof = ex.profile_table(batches=(1, 8, 32, 90), reps=3)
+        t1 = sum(L["runtime_ms"][0][1] for L in prof["components"][0]["layers"])
+        pool = 8
+        job = {"profile": prof, "workload": {"process": "poisson", "rate": 40000, "count": 400, "seed": 6,
+                                             "relative_deadline": 20 * t1},
+               "sim": {"scheduler": "ours-tardy", "granularity": "layer"}, "image_pool": pool, "image_seed": 4,
+               "pipeline_depth": 4, "dump_ids": list(range(1, 401, 7))}
+        r = ex.serve(job)
+        assert r["completed"] + r["dropped"] == 400 and r["h2d_bytes"] == 0
+        assert max(int(k) for k in r["step_members_hist"]) > 8  # batched steps
+        orc = NetOracle(ex.desc, 0, ex.weights())
+        assert _check_live_outputs(ex, r, 4, pool, [orc], limit=30) >= 20
 
 
 def test_live_serve_collab_config5():

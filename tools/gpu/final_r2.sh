@@ -1,5 +1,10 @@
-# Round-2 evidence: every bench config, the bench launch list, a full ncu capture of the top conv shapes.
-mkdir -p gpurun_out/final
+# Round-2 evidence: GPU tests, the reference-arm tables (bench.py's startup
+# table per config), every bench config (+ bf16, the reference arm), the bench
+# launch list, a full ncu capture of the top conv shapes.
+mkdir -p gpurun_out/final/tables
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/final/gputests.log 2>&1; echo "rc=$?" >> gpurun_out/final/gputests.log
+timeout 1500 python tools/bench_tables.py gpurun_out/final/tables > gpurun_out/final/tables.log 2>&1
+cp gpurun_out/final/tables/*_table_b200.json profiles/r02/
 for cfg in 2 1 3 4 5; do
   timeout 900 python bench.py --config $cfg > gpurun_out/final/bench_config$cfg.json 2> gpurun_out/final/bench_config$cfg.err
 done
