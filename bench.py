@@ -51,9 +51,22 @@ def dist_init():
     if ws > 1:
         import torch
         import torch.distributed as dist
+        # BENCH_ONE_DEVICE=1 + BENCH_DIST_BACKEND=gloo: every rank on GPU 0, a
+        # functional check of the N > 1 path on a one-GPU box (its timings
+        # mean nothing: the ranks share one GPU).
+        if os.environ.get("BENCH_ONE_DEVICE") == "1":
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group(_backend(), init_method="env://")
     return ws, rank, local
+
+
+def _backend() -> str:
+    return os.environ.get("BENCH_DIST_BACKEND", "nccl")
+
+
+def _red_device() -> str:
+    return "cpu" if _backend() == "gloo" else "cuda"
 
 
 def allreduce_max(x: float, ws: int) -> float:
@@ -61,7 +74,7 @@ def allreduce_max(x: float, ws: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_red_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -71,7 +84,7 @@ def allreduce_sum(x: float, ws: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_red_device())
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -193,8 +206,11 @@ def run_ours(a, ws, rank, local) -> dict | None:
     def dnn_ms(d, b):
         return sum(dict(L["runtime_ms"])[b] for cid in d["stages"] for L in comp[cid]["layers"])
 
-    t1 = max(dnn_ms(d, 1) for d in prof["dnns"])
-    tmax = max(dnn_ms(d, mb) for d in prof["dnns"])
+    # Every rank measures its own table (independent servers), but the rates
+    # probed must be the same on every rank (one global trace, sharded): start
+    # the capacity search from the slowest rank's table.
+    t1 = allreduce_max(max(dnn_ms(d, 1) for d in prof["dnns"]), ws)
+    tmax = allreduce_max(max(dnn_ms(d, mb) for d in prof["dnns"]), ws)
     # D = 6.25 x T1 (the paper's 150 ms / 24 ms ratio), T1 =
     # the single-request latency of the slowest DNN in the committed B200
     # table of this config (profiles/r02, measured by this executor; the
@@ -445,10 +461,12 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "measured": "bench.py startup on one B200 (per-layer events inside back-to-back passes scaled to the whole-pass time, median of 10)",
             "precision": a.precision, "suite": cfg["suite"]}), indent=1))
     try:
-        out["cpu_baseline"] = reference_baseline(job(cap, a.requests, 0), cap, 2, 5000)
+        # rank 0 at N = 1 only (at N > 1 the reference arm's own run carries it)
+        out["cpu_baseline"] = (reference_baseline(job(cap, a.requests, 0), cap, 2, 5000) if ws == 1 else
+                               {"unavailable": "reported at N = 1 only"})
     except Exception as e:  # the oracle binary is built where the reference is mounted
         out["cpu_baseline"] = {"unavailable": str(e)[:200]}
-    out["cpu_forward_img_s"] = cpu_forward(cfg["suite"]) if (a.config == 2 and a.cpu_forward) else None
+    out["cpu_forward_img_s"] = cpu_forward(cfg["suite"]) if (a.config == 2 and a.cpu_forward and ws == 1) else None
     return out
 
 

@@ -64,6 +64,8 @@ struct ReplayHook : batchsim::StepHook {
   int classes = 0;
   std::vector<float> host_img;
   int max_batch_seen = 0;
+  int rider_steps = 0;  // steps carrying >= 1 foreign request through a shared stage
+  int riders_total = 0;
   long steps = 0;
 
   bool log = std::getenv("BS_REPLAY_LOG") != nullptr;
@@ -92,6 +94,8 @@ struct ReplayHook : batchsim::StepHook {
     }
     ex->step(v.plan, v.segment, dnn_map[static_cast<std::size_t>(v.dnn)], v.from, v.to, v.members, v.riders);
     max_batch_seen = std::max(max_batch_seen, static_cast<int>(v.members.size() + v.riders.size()));
+    if (!v.riders.empty()) ++rider_steps;
+    riders_total += static_cast<int>(v.riders.size());
     ++steps;
   }
   void step_done(const batchsim::StepView&, const std::vector<batchsim::RequestId>& dep) override {
@@ -369,7 +373,8 @@ int bs_replay(bs_handle* h, const char* job_json, char** out) {
     json sm = batchsim::summary_to_json(res.metrics);
     sm["wall_ms"] = wall_ms;
     os << json{{"ev", "results"}, {"top1", top1}, {"probs", dumped}, {"launches", ex.launches() - launches0},
-               {"steps", hook.steps}, {"max_step_batch", hook.max_batch_seen}}
+               {"steps", hook.steps}, {"max_step_batch", hook.max_batch_seen},
+               {"rider_steps", hook.rider_steps}, {"riders", hook.riders_total}}
               .dump()
        << '\n';
     os << sm.dump() << '\n';

@@ -274,6 +274,34 @@ def test_hetero3_replay_config4():
         assert set(seen) == {0, 1, 2} and checked == 6
 
 
+def test_pair_replay_config3():
+    """Config 3: two DNNs sharing the ResNet-50 backbone, Pareto arrivals,
+    scheduler-driven shared-layer merges (foreign requests ride the other
+    DNN's backbone segment, inc/multi_dnn.hpp:291-301, deposited at the stage
+    end, inc/simulator.hpp:497-511); every step runs on the GPU and EVERY
+    served request matches the oracle of its own DNN."""
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("resnet50_pair", max_batch=90, max_requests=64) as ex:
+        w = ex.weights()
+        orcs = [NetOracle(ex.desc, k, w) for k in range(2)]
+        names = [n["name"] for n in ex.desc["nets"]]
+        count = 24
+        job = {"profile": synth_profile(ex, 1.0, 0.02),
+               "workload": {"process": "pareto", "rate": 400, "count": count, "seed": 7,
+                            "dnn_mix": [[n, 0.5] for n in names]},
+               "sim": {"scheduler": "ours-time", "granularity": "group", "max_batch": 90,
+                       "shared_batching": True},
+               "image_seed": 4, "dump_ids": list(range(1, count + 1))}
+        out = ex.replay(job)
+        summ = next(r for r in out if r["ev"] == "summary")
+        res = next(r for r in out if r["ev"] == "results")
+        assert summ["completed"] == count
+        assert res["max_step_batch"] > 1
+        assert res["rider_steps"] > 0 and res["riders"] > 0, res
+        seen, checked = _check_replay_outputs(ex, out, 4, orcs, per_dnn=count)
+        assert set(seen) == {0, 1} and checked == count
+
+
 def test_collab_partial_replay_config5():
     """Config 5: collaborative partial offload (client prefix of k layer
     groups, server suffix from the entry layer), Pareto arrivals, the LTE
