@@ -378,7 +378,17 @@ def run_ours(a, ws, rank, local) -> dict | None:
         roof["avg_launch_us"] = round(conv["ms"] / conv["launches"] * 1000, 2)
         roof["peak_source"] = (f"{pk['source']}: " + ("bf16_tflops_sustained" if a.precision == "bf16" else
                                "tf32 = bf16_tflops_sustained / 2") + "; hbm_gbs measured copy")
-        roof["traffic"] = ncu_traffic()
+        # DRAM bytes per launch: ncu's dram read + write over every conv_tc launch
+        # of the config-2 workload replayed at capacity, as a ratio to the
+        # algorithmic bytes of the same launches (profiles/ncu_conv_summary.json),
+        # applied to this run's algorithmic bytes per launch (the launch mixes
+        # differ; the ratio is the comparable figure). < 1: activations written
+        # by one layer are read from L2 by the next.
+        tr = ncu_traffic()
+        alg_per_launch = conv["bytes"] / conv["launches"]
+        roof["traffic"] = round(tr * alg_per_launch, 1) if tr is not None else None
+        roof["traffic_over_algorithmic"] = round(tr, 4) if tr is not None else None
+        roof["algorithmic_bytes_per_launch"] = round(alg_per_launch, 1)
         # The TF32 MMA rate measured on this part (profiles/r01/micro_b200.txt,
         # tools/micro/mma_micro.cu: one 128x128x8 MMA per 64 cycles per SM) at
         # the SM clock sampled during the run. 2xTF32 issues two MMAs per
@@ -471,11 +481,12 @@ def run_ours(a, ws, rank, local) -> dict | None:
 
 
 def ncu_traffic():
-    """dram bytes per launch of the conv kernel from the committed ncu capture."""
+    """DRAM bytes / algorithmic bytes of conv_tc launches from the committed ncu
+    launch list (tools/traffic_replay.py, tools/traffic_summary.py)."""
     f = ROOT / "profiles" / "ncu_conv_summary.json"
     if f.exists():
         try:
-            return json.loads(f.read_text()).get("dram_bytes_per_launch")
+            return json.loads(f.read_text()).get("dram_over_algorithmic")
         except Exception:
             return None
     return None
