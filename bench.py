@@ -316,27 +316,47 @@ def run_ours(a, ws, rank, local) -> dict | None:
     # Same metric: served req/s at a rate where the on-time ratio still meets
     # 0.90. Starts at the device-resident rate and steps down (step_down) when
     # the H2D admission path cannot hold the deadlines there.
+    def e2e_run(rate):
+        c = on = gen = hb = db = 0
+        ms = 0.0
+        barrier(ws)
+        for k in range(a.steps):
+            r = ex.serve(job(rate, a.requests, 5000 + k, h2d=True))
+            c += r["completed"]
+            on += r["on_time"]
+            gen += r["generated"]
+            ms += r["device_ms"]
+            hb += r["h2d_bytes"]
+            db += r["d2h_bytes"]
+        barrier(ws)
+        return {"rate": rate, "completed": c, "ms": ms, "h2d": hb, "d2h": db,
+                "ratio": allreduce_sum(on, ws) / max(1.0, allreduce_sum(gen, ws))}
+
     e2e_cap = cap
     e2e_steps_down = []
     for attempt in range(7):
-        e2e_completed = e2e_on = e2e_gen = 0
-        e2e_ms = 0.0
-        h2d = d2h = 0
-        barrier(ws)
-        for k in range(a.steps):
-            r = ex.serve(job(e2e_cap, a.requests, 5000 + k, h2d=True))
-            e2e_completed += r["completed"]
-            e2e_on += r["on_time"]
-            e2e_gen += r["generated"]
-            e2e_ms += r["device_ms"]
-            h2d += r["h2d_bytes"]
-            d2h += r["d2h_bytes"]
-        barrier(ws)
-        e2e_ratio = allreduce_sum(e2e_on, ws) / max(1.0, allreduce_sum(e2e_gen, ws))
-        if e2e_ratio >= 0.90 or attempt == 6:
+        run = e2e_run(e2e_cap)
+        if run["ratio"] >= 0.90 or attempt == 6:
             break
-        e2e_steps_down.append([round(e2e_cap, 1), round(e2e_ratio, 4)])
-        e2e_cap = step_down(e2e_cap, e2e_ratio)
+        e2e_steps_down.append([round(e2e_cap, 1), round(run["ratio"], 4)])
+        e2e_cap = step_down(e2e_cap, run["ratio"])
+    # After a coarse step-down (15% / 30%) the capacity lies between the last
+    # failing and the passing rate: up to three bisections, keeping the
+    # highest passing rate's runs (the same capacity rule as the device path).
+    if e2e_steps_down and run["ratio"] >= 0.90:
+        lo, hi = e2e_cap, e2e_steps_down[-1][0]
+        for _ in range(3):
+            if hi / lo < 1.04:
+                break
+            mid = (lo * hi) ** 0.5
+            trial = e2e_run(mid)
+            if trial["ratio"] >= 0.90:
+                run, lo = trial, mid
+            else:
+                e2e_steps_down.append([round(mid, 1), round(trial["ratio"], 4)])
+                hi = mid
+        e2e_cap = run["rate"]
+    e2e_completed, e2e_ms, h2d, d2h, e2e_ratio = run["completed"], run["ms"], run["h2d"], run["d2h"], run["ratio"]
 
     # The deadline rule applied to today's executor: D = 6.25 x T1 of the
     # startup table (tighter as single-request latency improves). Capacity

@@ -53,6 +53,10 @@ Executor::Executor(int device, const std::string& suite_name, int max_batch, int
     staging_floats_ = (mx + 63) / 64 * 64;
     staging_n_ = 64;
     ck(cudaMalloc(&staging_, staging_floats_ * staging_n_), "rgb staging");
+    ck(cudaMallocHost(&pack_host_, staging_floats_ * staging_n_), "rgb pack");
+    pack_seq_.assign(static_cast<std::size_t>(staging_n_), 0);
+    pack_ev_.resize(128);
+    for (auto& e : pack_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "pack event");
   }
   // One slot space: [request slots | ride buffers | profiler scratch], so a
   // single TMA tensor map per layer input addresses every blob by slot index.
@@ -269,6 +273,8 @@ Executor::~Executor() {
   for (cudaEvent_t e : ready_ring_) cudaEventDestroy(e);
   for (cudaEvent_t e : free_ring_) cudaEventDestroy(e);
   cudaFree(staging_);
+  cudaFreeHost(pack_host_);
+  for (cudaEvent_t e : pack_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   for (float* p : pool_) cudaFree(p);
   cudaFree(d_weights_);
@@ -657,6 +663,68 @@ void Executor::admit_rgb(std::int64_t id, int dnn, const std::uint8_t* rgb) {
   s.ready_seq = ++ready_seq_;
   s.ready_stream = 0;
   slot_of_.emplace(id, s);
+}
+
+void Executor::admit_rgb_many(const std::int64_t* ids, int dnn, const std::uint8_t* const* rgb, int k) {
+  if (k <= 0) return;
+  const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
+  const TensorDef& in = net.tensors[static_cast<std::size_t>(net.input_t)];
+  if (in.C != 4) throw std::invalid_argument("admit_rgb needs a 4-channel padded input");
+  const int hw = in.H * in.W;
+  const std::size_t bytes = static_cast<std::size_t>(hw) * 3;
+  for (int i = 0; i < k; ++i)
+    if (slot_of_.count(ids[i])) throw std::logic_error("request admitted twice: " + std::to_string(ids[i]));
+  if (free_.size() < static_cast<std::size_t>(k)) throw std::runtime_error("activation arena full");
+  int done = 0;
+  while (done < k) {
+    // consecutive staging slots (no wrap inside one copy), at most kExpandMax
+    const int first = staging_next_;
+    const int take = std::min({k - done, staging_n_ - first, kExpandMax});
+    // The host regions were last read by earlier batches' H2D copies on copy_
+    // (in order): waiting for the newest of them covers the rest.
+    long newest = 0;
+    for (int q = 0; q < take; ++q) newest = std::max(newest, pack_seq_[static_cast<std::size_t>(first + q)]);
+    if (newest > pack_synced_) {
+      ck(cudaEventSynchronize(pack_ev_[static_cast<std::size_t>(newest % 128)]), "pack reuse");
+      pack_synced_ = newest;
+    }
+    std::uint8_t* host = pack_host_ + static_cast<std::size_t>(first) * staging_floats_;
+    std::uint8_t* dev = staging_ + static_cast<std::size_t>(first) * staging_floats_;
+    for (int q = 0; q < take; ++q) std::memcpy(host + static_cast<std::size_t>(q) * staging_floats_, rgb[done + q], bytes);
+    ck(cudaMemcpyAsync(dev, host, static_cast<std::size_t>(take - 1) * staging_floats_ + bytes, cudaMemcpyHostToDevice,
+                       copy_), "admit rgb batch H2D");
+    const long seq = ++pack_batches_;
+    ck(cudaEventRecord(pack_ev_[static_cast<std::size_t>(seq % 128)], copy_), "pack rec");
+    for (int q = 0; q < take; ++q) pack_seq_[static_cast<std::size_t>(first + q)] = seq;
+    staging_next_ = (first + take) % staging_n_;
+    ExpandManyParams ep;
+    ep.rgb = dev;
+    ep.stride = static_cast<long>(staging_floats_);
+    ep.hw = hw;
+    ep.n = take;
+    std::vector<Slot> slots(static_cast<std::size_t>(take));
+    for (int q = 0; q < take; ++q) {
+      Slot& s = slots[static_cast<std::size_t>(q)];
+      s.index = free_.back();
+      free_.pop_back();
+      s.dnn = dnn;
+      s.blob = slot_ptr(s.index);
+      wait_slot_free(s.index, copy_);
+      ep.dst[q] = s.blob + in.off;
+    }
+    ck(launch_expand_rgb_many(ep, copy_), "expand rgb batch");
+    const cudaEvent_t ready = next_ready_event();
+    ck(cudaEventRecord(ready, copy_), "ready rec");
+    for (int q = 0; q < take; ++q) {
+      Slot& s = slots[static_cast<std::size_t>(q)];
+      s.ready = ready;
+      s.pending_ready = true;
+      s.ready_seq = ++ready_seq_;
+      s.ready_stream = 0;
+      slot_of_.emplace(ids[done + q], s);
+    }
+    done += take;
+  }
 }
 
 void Executor::wait_ready(const std::vector<Slot*>& pending) {

@@ -59,6 +59,11 @@ class Executor {
   // padded fp32 input tensor on the device; the request's first step waits
   // for it (copies overlap compute).
   void admit_rgb(std::int64_t id, int dnn, const std::uint8_t* rgb_pinned);
+  // k images of one DNN admitted together: packed into a pinned staging
+  // region on the host, one H2D copy, one expansion launch and one ready event
+  // for the batch (for small images, where per-request copies, launches and
+  // events bound the host loop).
+  void admit_rgb_many(const std::int64_t* ids, int dnn, const std::uint8_t* const* rgb, int k);
   // Device-resident input (e.g. an image pool in HBM) admitted by reference:
   // no copy into the blob and no admission event; the request's first layer
   // reads its input tensor straight from `image` (same NHWC layout), which
@@ -204,6 +209,10 @@ class Executor {
   std::uint8_t* staging_ = nullptr;  // 8-bit RGB staging ring
   std::size_t staging_floats_ = 0;      // bytes per staging slot
   int staging_n_ = 0, staging_next_ = 0;
+  std::uint8_t* pack_host_ = nullptr;  // pinned host mirror of the staging ring (batched admissions)
+  std::vector<long> pack_seq_;         // per staging slot: batch that last copied from its host region
+  std::vector<cudaEvent_t> pack_ev_;   // per batch (ring of 128): its H2D copy is done
+  long pack_batches_ = 0, pack_synced_ = 0;
   cudaEvent_t next_ready_event();
   long ready_seq_ = 0;
   // One stream wait per admission stream for the pending members / riders

@@ -485,6 +485,19 @@ __global__ void expand_rgb_kernel(const unsigned char* __restrict__ rgb, float* 
   }
 }
 
+__global__ void expand_rgb_many_kernel(const ExpandManyParams p) {
+  pdl::launch_dependents();
+  pdl::wait();
+  const unsigned char* __restrict__ rgb = p.rgb + blockIdx.y * p.stride;
+  float* __restrict__ dst = p.dst[blockIdx.y];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.hw; i += gridDim.x * blockDim.x) {
+    const float r = (static_cast<int>(rgb[3 * i]) - 128) * (1.0f / 32.0f);
+    const float g = (static_cast<int>(rgb[3 * i + 1]) - 128) * (1.0f / 32.0f);
+    const float b = (static_cast<int>(rgb[3 * i + 2]) - 128) * (1.0f / 32.0f);
+    reinterpret_cast<float4*>(dst)[i] = make_float4(r, g, b, 0.f);
+  }
+}
+
 __global__ void to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, std::size_t n) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
@@ -505,6 +518,14 @@ cudaError_t launch_expand_rgb(const unsigned char* rgb, float* dst, int hw, cuda
   pdl::suppress_next();  // admission copy stream: after an H2D copy / event wait
   e = pdl::launch(expand_rgb_kernel, dim3(grid_for(hw)), dim3(kThreads), 0, s, rgb, dst, hw);
   return e;
+}
+
+cudaError_t launch_expand_rgb_many(const ExpandManyParams& p, cudaStream_t s) {
+  if (p.n <= 0) return cudaSuccess;
+  if (p.n > kExpandMax) return cudaErrorInvalidValue;
+  pdl::suppress_next();  // admission copy stream: after an H2D copy / event wait
+  const unsigned bx = static_cast<unsigned>(std::min<long>(grid_for(p.hw), 16));
+  return pdl::launch(expand_rgb_many_kernel, dim3(bx, p.n), dim3(kThreads), 0, s, p);
 }
 
 cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {

@@ -56,6 +56,16 @@ struct SoftmaxParams {
 // 8-bit packed RGB [hw][3] -> padded fp32 [hw][4] with value (b - 128) / 32
 // (the synthetic images' pixel encoding, csrc/exec/image.hpp).
 cudaError_t launch_expand_rgb(const unsigned char* rgb, float* dst, int hw, cudaStream_t s);
+// The same for k <= kExpandMax images packed at `stride` bytes in one staging
+// region (one launch per batch of small admitted images).
+constexpr int kExpandMax = 64;
+struct ExpandManyParams {
+  const unsigned char* rgb;
+  long stride;
+  int hw, n;
+  float* dst[kExpandMax];
+};
+cudaError_t launch_expand_rgb_many(const ExpandManyParams& p, cudaStream_t s);
 cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s);
 cudaError_t launch_avgpool(const AvgPoolParams& p, cudaStream_t s);
 cudaError_t launch_dwconv(const DwParams& p, cudaStream_t s);

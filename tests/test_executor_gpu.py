@@ -470,6 +470,35 @@ def test_live_serve_h2d_outputs_match_oracle():
         assert _check_live_outputs(ex, r, 4, pool, [orc]) >= 4
 
 
+def test_live_serve_h2d_batched_admission_small_cnn():
+    """Small images (SmallCNN, 3 KB of 8-bit RGB) are admitted in batches per
+    loop iteration (one packed H2D copy, one expansion launch, one ready event
+    per batch, Executor::admit_rgb_many) at a rate where many arrive per
+    iteration; served probabilities match the oracle, and the per-request
+    path (BS_BATCH_ADMIT_BYTES=0) serves the same outputs."""
+    import os
+    from paper_2304_09961_b200.executor import Executor
+    with Executor("small_cnn", max_batch=10, max_requests=1024) as ex:
+        prof = ex.profile_table(batches=(1, 2, 4, 8, 10), reps=3)
+        t1 = sum(L["runtime_ms"][0][1] for L in prof["components"][0]["layers"])
+        pool = 16
+        job = {"profile": prof, "workload": {"process": "poisson", "rate": 60000, "count": 2000, "seed": 8,
+                                             "relative_deadline": 40 * t1},
+               "sim": {"scheduler": "ours-time", "granularity": "request", "max_batch": 10}, "image_pool": pool,
+               "image_seed": 4, "h2d": True, "pipeline_depth": 4, "dump_ids": list(range(1, 2001, 13))}
+        r = ex.serve(job)
+        assert r["completed"] + r["dropped"] == 2000 and r["h2d_bytes"] == 2000 * 32 * 32 * 3
+        orc = NetOracle(ex.desc, 0, ex.weights())
+        assert _check_live_outputs(ex, r, 4, pool, [orc], limit=60) >= 40
+        os.environ["BS_BATCH_ADMIT_BYTES"] = "0"
+        try:
+            r1 = ex.serve(dict(job, workload=dict(job["workload"], count=300), dump_ids=list(range(1, 301, 7))))
+        finally:
+            del os.environ["BS_BATCH_ADMIT_BYTES"]
+        assert r1["completed"] + r1["dropped"] == 300
+        assert _check_live_outputs(ex, r1, 4, pool, [orc], limit=40) >= 20
+
+
 def test_live_serve_device_resident_outputs_match_oracle():
     """The bench's `value` path: HBM-resident pool images admitted by
     reference (layer 1 reads each image in place, no admission copy), at a
