@@ -100,6 +100,17 @@ int bs_admit(bs_handle* h, int64_t id, int dnn, int entry_layer, const float* im
  * the image in place, so it must stay valid and unchanged until that layer
  * has run (e.g. until the request retires). */
 int bs_admit_device(bs_handle* h, int64_t id, int dnn, const float* image_device);
+/* Arrivals shipped as packed 8-bit RGB [H][W][3] (value (byte - 128) / 32,
+ * csrc/exec/image.hpp) in PINNED host memory, for DNNs with a 4-channel padded
+ * input: H2D on the handle's admission stream into a staging ring, expanded
+ * on the device into the request's input tensor; its first step waits for it.
+ * The caller keeps `rgb` unchanged until the copy has run (the next
+ * bs_step_ex's done event covers it). */
+int bs_admit_rgb(bs_handle* h, int64_t id, int dnn, const uint8_t* rgb_pinned);
+/* k arrivals of one DNN at once (any host memory): packed into a pinned staging
+ * region, one H2D copy, one expansion launch and one ready event for the
+ * batch -- for small images, where per-request copies bound the host loop. */
+int bs_admit_rgb_many(bs_handle* h, const int64_t* ids, int dnn, const uint8_t* const* rgb, int k);
 int bs_plan(bs_handle* h, int plan_no);
 int bs_step(bs_handle* h, int plan_no, int segment, int dnn, int layer_from, int layer_to,
             const bs_member* members, int n_members, const bs_rider* riders, int n_riders);

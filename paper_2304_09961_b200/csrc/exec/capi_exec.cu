@@ -195,6 +195,22 @@ int bs_admit_device(bs_handle* h, int64_t id, int dnn, const float* image_device
   });
 }
 
+int bs_admit_rgb(bs_handle* h, int64_t id, int dnn, const uint8_t* rgb_pinned) {
+  return guarded([&] {
+    if (!rgb_pinned) throw std::invalid_argument("bs_admit_rgb: null image");
+    h->ex->admit_rgb(id, dnn, rgb_pinned);
+    return BS_OK;
+  });
+}
+
+int bs_admit_rgb_many(bs_handle* h, const int64_t* ids, int dnn, const uint8_t* const* rgb, int k) {
+  return guarded([&] {
+    if (k < 0 || (k > 0 && (!ids || !rgb))) throw std::invalid_argument("bs_admit_rgb_many: bad arrays");
+    h->ex->admit_rgb_many(ids, dnn, rgb, k);
+    return BS_OK;
+  });
+}
+
 int bs_plan(bs_handle* h, int plan_no) {
   return guarded([&] {
     h->ex->new_plan(plan_no);

@@ -178,6 +178,17 @@ class Executor:
         it must outlive that layer."""
         _check(_lib().bs_admit_device(self._h, rid, dnn, C.c_void_p(image_ptr)))
 
+    def admit_rgb_many(self, rids, dnn: int, images):
+        """Admit k arrivals of one DNN shipped as packed 8-bit RGB [H][W][3]
+        uint8 arrays (bs_admit_rgb_many: one packed H2D copy and one
+        expansion launch for the batch)."""
+        import numpy as np
+        arrs = [np.ascontiguousarray(im, dtype=np.uint8) for im in images]
+        k = len(arrs)
+        ids = (C.c_int64 * k)(*rids)
+        ptrs = (C.c_void_p * k)(*[a.ctypes.data for a in arrs])
+        _check(_lib().bs_admit_rgb_many(self._h, ids, dnn, ptrs, k))
+
     def plan(self, plan_no: int):
         _check(_lib().bs_plan(self._h, plan_no))
 

@@ -96,6 +96,24 @@ def test_admit_device_reads_input_in_place(googlenet):
         assert np.array_equal(t.cpu().numpy(), imgs[i])
 
 
+def test_admit_rgb_many_boundary(googlenet):
+    """bs_admit_rgb_many: arrivals shipped as packed 8-bit RGB, admitted as one
+    batch (one packed H2D copy, one expansion launch), stepped in one ragged
+    step with a copied fp32 admission -- outputs match the oracle."""
+    ex, w = googlenet
+    orc = NetOracle(ex.desc, 0, w)
+    imgs = {i: image_for(ex, 0, i) for i in (301, 302, 303, 304)}
+    rgb = {i: np.rint(im[..., :3] * 32.0 + 128.0).astype(np.uint8) for i, im in imgs.items()}
+    for i in rgb:  # the synthetic images are exactly byte / 32 - 4
+        assert np.array_equal((rgb[i].astype(np.float32) - 128.0) / 32.0, imgs[i][..., :3])
+    ex.admit_rgb_many([301, 302, 303], 0, [rgb[301], rgb[302], rgb[303]])
+    ex.admit(304, 0, imgs[304])
+    ex.plan(3)
+    ex.step(3, 0, 0, 1, 22, [(301, 1), (302, 1), (303, 1), (304, 1)])
+    for i in imgs:
+        assert_request_matches(ex.retire(i, 1000), orc.probs(orc.forward(imgs[i])), TOL)
+
+
 def test_googlenet_full_batch_90(googlenet):
     ex, w = googlenet
     orc = NetOracle(ex.desc, 0, w)
