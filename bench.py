@@ -233,7 +233,17 @@ def run_ours(a, ws, rank, local) -> dict | None:
     # 0.83-0.87 at 3 and 0.81-0.86 at 6, 0.75-0.81 at 8 (deeper plans further
     # ahead of the arrivals), configs 1 / 3 / 4 neutral
     # (profiles/r02/serving_steps/depth_*.txt)
-    base = dict(collab_inputs(cfg), profile=prof, sim=sim, image_pool=64, pipeline_depth=depth)
+    # Planning margin (A/B switch, default 1.0 = plan on the measured table):
+    # every h_k(b) the scheduler sees is scaled by it.
+    margin = float(os.environ.get("BENCH_TABLE_MARGIN", cfg.get("table_margin", 1.0)))
+    plan_prof = prof
+    if margin != 1.0:
+        import copy
+        plan_prof = copy.deepcopy(prof)
+        for c in plan_prof["components"]:
+            for L in c["layers"]:
+                L["runtime_ms"] = [[b, ms * margin] for b, ms in L["runtime_ms"]]
+    base = dict(collab_inputs(cfg), profile=plan_prof, sim=sim, image_pool=64, pipeline_depth=depth)
 
     def job(rate, count, seed, h2d=False, dl=None):
         """One serving run. N > 1: ONE global trace (N x the per-GPU rate and
@@ -460,6 +470,7 @@ def run_ours(a, ws, rank, local) -> dict | None:
             "precision": a.precision,
             "pdl": pdl_on,
             "pipeline_depth": int(os.environ.get("BENCH_DEPTH", cfg.get("depth", 4))),
+            "table_margin": margin,
             "latency_table": "cold L2 (flushed before every timed layer)" if a.table_flush_l2 else
                              f"warm L2, timing '{table_timing(cfg)}' (median of back-to-back repetitions)",
             "l2": "no flush: each step touches R x 4.6 MB request blobs (>> 126 MB L2) plus 26 MB of weights",
