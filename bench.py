@@ -823,7 +823,8 @@ def main() -> None:
     ap.add_argument("--warm-requests", type=int, default=3000, help="requests per capacity-search run")
     ap.add_argument("--slots", type=int, default=4096, help="activation-arena slots")
     ap.add_argument("--precision", default="tf32x2", choices=["tf32x2", "tf32", "bf16"])
-    ap.add_argument("--stats-every", type=int, default=4)
+    ap.add_argument("--stats-every", type=int, default=32,
+                    help="sample every Nth launch with CUDA events in the timed region (every 4th cost ~13%% of config 2 capacity: an event between two kernels breaks their programmatic launch)")
     ap.add_argument("--cpu-forward", type=int, default=1, help="time the CPU fp32 forward at b = 1 / 10 / 90")
     ap.add_argument("--dump-table", default=None, help="write the measured latency table here")
     ap.add_argument("--table-flush-l2", type=int, default=0,
