@@ -665,7 +665,7 @@ void Executor::admit_rgb(std::int64_t id, int dnn, const std::uint8_t* rgb) {
   slot_of_.emplace(id, s);
 }
 
-void Executor::admit_rgb_many(const std::int64_t* ids, int dnn, const std::uint8_t* const* rgb, int k) {
+void Executor::admit_rgb_many(const std::int64_t* ids, int dnn, const std::uint8_t* const* rgb, int k, bool pinned_src) {
   if (k <= 0) return;
   const NetDef& net = suite_.nets[static_cast<std::size_t>(dnn)];
   const TensorDef& in = net.tensors[static_cast<std::size_t>(net.input_t)];
@@ -682,20 +682,26 @@ void Executor::admit_rgb_many(const std::int64_t* ids, int dnn, const std::uint8
     const int take = std::min({k - done, staging_n_ - first, kExpandMax});
     // The host regions were last read by earlier batches' H2D copies on copy_
     // (in order): waiting for the newest of them covers the rest.
-    long newest = 0;
-    for (int q = 0; q < take; ++q) newest = std::max(newest, pack_seq_[static_cast<std::size_t>(first + q)]);
-    if (newest > pack_synced_) {
-      ck(cudaEventSynchronize(pack_ev_[static_cast<std::size_t>(newest % 128)]), "pack reuse");
-      pack_synced_ = newest;
-    }
-    std::uint8_t* host = pack_host_ + static_cast<std::size_t>(first) * staging_floats_;
     std::uint8_t* dev = staging_ + static_cast<std::size_t>(first) * staging_floats_;
-    for (int q = 0; q < take; ++q) std::memcpy(host + static_cast<std::size_t>(q) * staging_floats_, rgb[done + q], bytes);
-    ck(cudaMemcpyAsync(dev, host, static_cast<std::size_t>(take - 1) * staging_floats_ + bytes, cudaMemcpyHostToDevice,
-                       copy_), "admit rgb batch H2D");
-    const long seq = ++pack_batches_;
-    ck(cudaEventRecord(pack_ev_[static_cast<std::size_t>(seq % 128)], copy_), "pack rec");
-    for (int q = 0; q < take; ++q) pack_seq_[static_cast<std::size_t>(first + q)] = seq;
+    if (pinned_src) {
+      for (int q = 0; q < take; ++q)
+        ck(cudaMemcpyAsync(dev + static_cast<std::size_t>(q) * staging_floats_, rgb[done + q], bytes,
+                           cudaMemcpyHostToDevice, copy_), "admit rgb H2D");
+    } else {
+      long newest = 0;
+      for (int q = 0; q < take; ++q) newest = std::max(newest, pack_seq_[static_cast<std::size_t>(first + q)]);
+      if (newest > pack_synced_) {
+        ck(cudaEventSynchronize(pack_ev_[static_cast<std::size_t>(newest % 128)]), "pack reuse");
+        pack_synced_ = newest;
+      }
+      std::uint8_t* host = pack_host_ + static_cast<std::size_t>(first) * staging_floats_;
+      for (int q = 0; q < take; ++q) std::memcpy(host + static_cast<std::size_t>(q) * staging_floats_, rgb[done + q], bytes);
+      ck(cudaMemcpyAsync(dev, host, static_cast<std::size_t>(take - 1) * staging_floats_ + bytes, cudaMemcpyHostToDevice,
+                         copy_), "admit rgb batch H2D");
+      const long seq = ++pack_batches_;
+      ck(cudaEventRecord(pack_ev_[static_cast<std::size_t>(seq % 128)], copy_), "pack rec");
+      for (int q = 0; q < take; ++q) pack_seq_[static_cast<std::size_t>(first + q)] = seq;
+    }
     staging_next_ = (first + take) % staging_n_;
     ExpandManyParams ep;
     ep.rgb = dev;

@@ -63,7 +63,10 @@ class Executor {
   // region on the host, one H2D copy, one expansion launch and one ready event
   // for the batch (for small images, where per-request copies, launches and
   // events bound the host loop).
-  void admit_rgb_many(const std::int64_t* ids, int dnn, const std::uint8_t* const* rgb, int k);
+  // pinned_src: the images are in pinned host memory -- each is DMA'd straight
+  // into its staging slot (no host packing; for large images), and the batch
+  // still shares one expansion launch and one ready event.
+  void admit_rgb_many(const std::int64_t* ids, int dnn, const std::uint8_t* const* rgb, int k, bool pinned_src = false);
   // Device-resident input (e.g. an image pool in HBM) admitted by reference:
   // no copy into the blob and no admission event; the request's first layer
   // reads its input tensor straight from `image` (same NHWC layout), which

@@ -210,6 +210,12 @@ json serve_live(Executor& ex, const json& j) {
     const char* e = std::getenv("BS_BATCH_ADMIT_BYTES");
     return e ? std::atol(e) : 16384L;
   }();
+  // BS_BATCH_ADMIT_LARGE=1: larger images batched too (per-image DMA, shared
+  // expansion launch and ready event) -- A/B switch
+  const bool batch_admit_large = [] {
+    const char* e = std::getenv("BS_BATCH_ADMIT_LARGE");
+    return e && std::atoi(e) != 0;
+  }();
   std::vector<std::vector<RequestId>> batch_ids(ex.suite().nets.size());
   std::vector<std::vector<const std::uint8_t*>> batch_src(ex.suite().nets.size());
   cudaEvent_t dev0, dev1;
@@ -229,7 +235,7 @@ json serve_live(Executor& ex, const json& j) {
       const int img = static_cast<int>(i % static_cast<std::size_t>(pool));
       if (h2d && adm[ai].entry_layer == 1) {
         const std::uint8_t* src = host_pool[static_cast<std::size_t>(net)] + img_floats[static_cast<std::size_t>(net)] * img;
-        if (static_cast<long>(img_floats[static_cast<std::size_t>(net)]) <= batch_admit_bytes) {
+        if (static_cast<long>(img_floats[static_cast<std::size_t>(net)]) <= batch_admit_bytes || batch_admit_large) {
           batch_ids[static_cast<std::size_t>(net)].push_back(id);
           batch_src[static_cast<std::size_t>(net)].push_back(src);
         } else {
@@ -256,8 +262,11 @@ json serve_live(Executor& ex, const json& j) {
     // small images arrived in this iteration: one packed copy + expansion per DNN
     for (std::size_t q = 0; q < batch_ids.size(); ++q) {
       if (batch_ids[q].empty()) continue;
+      // images above the packing size come from the pinned pool: DMA'd one by
+      // one into consecutive staging slots, one expansion + event per batch
       ex.admit_rgb_many(batch_ids[q].data(), static_cast<int>(q), batch_src[q].data(),
-                        static_cast<int>(batch_ids[q].size()));
+                        static_cast<int>(batch_ids[q].size()),
+                        static_cast<long>(img_floats[q]) > batch_admit_bytes);
       batch_ids[q].clear();
       batch_src[q].clear();
     }
