@@ -431,7 +431,8 @@ int bs_stats_summary(bs_handle* h, double hbm_gbs, double tensor_tflops, char** 
     for (const LaunchStat& st : h->ex->stats()) {
       float ms = 0;
       if (cudaEventElapsedTime(&ms, st.t0, st.t1) != cudaSuccess) continue;
-      const char* k = st.kind == OpKind::conv      ? "conv_tc"
+      const char* k = st.gemv                      ? "fc_gemv"
+                      : st.kind == OpKind::conv    ? "conv_tc"
                       : st.kind == OpKind::maxpool ? "maxpool"
                       : st.kind == OpKind::avgpool ? "avgpool"
                       : st.kind == OpKind::dwconv  ? "dwconv"

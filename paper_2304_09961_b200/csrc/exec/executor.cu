@@ -521,7 +521,20 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
   cudaError_t e = cudaSuccess;
   switch (op.kind) {
     case OpKind::conv: {
-      e = launch_conv_tc(conv_params(net, op, d_ptrs, batch), stream_);
+      const ConvParams cp = conv_params(net, op, d_ptrs, batch);
+      // small-batch FC: weight-streaming GEMV (BS_FC_GEMV=0 keeps conv_tc)
+      static const bool gemv_on = [] {
+        const char* v = std::getenv("BS_FC_GEMV");
+        return !(v && std::atoi(v) == 0);
+      }();
+      if (gemv_on && prec_ != 2 && cp.H == 1 && cp.W == 1 && cp.KH == 1 && cp.KW == 1 && cp.nimg <= kFcMaxImg &&
+          !cp.res_ptrs && !cp.round_out && cp.in_off % 4 == 0 && cp.K % 4 == 0) {
+        FcParams fp{cp.nimg, cp.K, cp.Kpad, cp.N, cp.relu, cp.in_ptrs, cp.in_off, cp.wgt, cp.bias, cp.out_ptrs, cp.out_off};
+        st.gemv = true;
+        e = launch_fc_gemv(fp, stream_);
+      } else {
+        e = launch_conv_tc(cp, stream_);
+      }
       break;
     }
     case OpKind::maxpool: {

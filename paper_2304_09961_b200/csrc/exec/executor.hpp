@@ -33,6 +33,7 @@ struct LaunchStat {
   double bytes;   // algorithmic
   double flops;
   cudaEvent_t t0, t1;
+  bool gemv = false;  // a small-batch FC ran as the weight-streaming GEMV (not conv_tc)
 };
 
 struct RideKey {

@@ -528,6 +528,61 @@ cudaError_t launch_expand_rgb_many(const ExpandManyParams& p, cudaStream_t s) {
   return pdl::launch(expand_rgb_many_kernel, dim3(bx, p.n), dim3(kThreads), 0, s, p);
 }
 
+namespace {
+__global__ void __launch_bounds__(256) fc_gemv_kernel(const FcParams p) {
+  pdl::launch_dependents();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.x * 8 + warp;
+  const bool col = n < p.N;
+  const float* w = p.wgt + static_cast<long>(col ? n : 0) * p.Kpad;
+  // weights are immutable: the first slice is loaded before waiting for the
+  // previous kernel (the pooled inputs it writes)
+  float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (col && lane * 4 < p.K) w0 = __ldg(reinterpret_cast<const float4*>(w + lane * 4));
+  pdl::wait();
+  if (!col) return;
+  float acc[kFcMaxImg];
+  const float* a[kFcMaxImg];
+#pragma unroll
+  for (int m = 0; m < kFcMaxImg; ++m) {
+    acc[m] = 0.f;
+    a[m] = m < p.nimg ? p.in_ptrs[m] + p.in_off : nullptr;
+  }
+  for (int k = lane * 4; k < p.K; k += 128) {
+    const float4 w4 = k == lane * 4 ? w0 : __ldg(reinterpret_cast<const float4*>(w + k));
+#pragma unroll
+    for (int m = 0; m < kFcMaxImg; ++m) {
+      if (m < p.nimg) {
+        const float4 x = *reinterpret_cast<const float4*>(a[m] + k);
+        acc[m] = fmaf(x.x, w4.x, acc[m]);
+        acc[m] = fmaf(x.y, w4.y, acc[m]);
+        acc[m] = fmaf(x.z, w4.z, acc[m]);
+        acc[m] = fmaf(x.w, w4.w, acc[m]);
+      }
+    }
+  }
+  const float b = p.bias ? __ldg(p.bias + n) : 0.f;
+#pragma unroll
+  for (int m = 0; m < kFcMaxImg; ++m) {
+    if (m >= p.nimg) break;
+    float v = acc[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      v += b;
+      if (p.relu == 1) v = fmaxf(v, 0.f);
+      else if (p.relu == 2) v = fminf(fmaxf(v, 0.f), 6.f);
+      p.out_ptrs[m][p.out_off + n] = v;
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_fc_gemv(const FcParams& p, cudaStream_t s) {
+  if (p.nimg <= 0 || p.nimg > kFcMaxImg || p.K % 4 || p.Kpad % 4 || p.in_off % 4) return cudaErrorInvalidValue;
+  return pdl::launch(fc_gemv_kernel, dim3((p.N + 7) / 8), dim3(256), 0, s, p);
+}
+
 cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   if (p.C % 4 || p.k > 3) return cudaErrorInvalidValue;

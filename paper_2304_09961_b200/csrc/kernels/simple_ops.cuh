@@ -66,6 +66,22 @@ struct ExpandManyParams {
   float* dst[kExpandMax];
 };
 cudaError_t launch_expand_rgb_many(const ExpandManyParams& p, cudaStream_t s);
+// Fully connected layer at small batch (1x1 conv on a 1x1 input, nimg <=
+// kFcMaxImg): weight streaming GEMV, one warp per output column reading its
+// weight row once for every image of the batch, fp32 FMA accumulation. At
+// b <= 8 the tcgen05 tile is almost empty and the layer is a pure weight
+// stream (GoogLeNet's 4 MB, ResNet-50's 8 MB).
+constexpr int kFcMaxImg = 8;
+struct FcParams {
+  int nimg, K, Kpad, N, relu;
+  const float* const* in_ptrs;
+  long in_off;
+  const float* wgt;   // [N][Kpad]
+  const float* bias;  // [N] or nullptr
+  float* const* out_ptrs;
+  long out_off;
+};
+cudaError_t launch_fc_gemv(const FcParams& p, cudaStream_t s);
 cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s);
 cudaError_t launch_avgpool(const AvgPoolParams& p, cudaStream_t s);
 cudaError_t launch_dwconv(const DwParams& p, cudaStream_t s);
