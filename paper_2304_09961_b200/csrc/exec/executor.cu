@@ -528,7 +528,7 @@ void Executor::launch_op(const NetDef& net, const OpDef& op, float* const* d_ptr
         return !(v && std::atoi(v) == 0);
       }();
       if (gemv_on && prec_ != 2 && cp.H == 1 && cp.W == 1 && cp.KH == 1 && cp.KW == 1 && cp.nimg <= kFcMaxImg &&
-          !cp.res_ptrs && !cp.round_out && cp.in_off % 4 == 0 && cp.K % 4 == 0) {
+          !cp.res_ptrs && !cp.round_out && cp.in_off % 4 == 0 && cp.K % 4 == 0 && cp.K <= 4096) {
         FcParams fp{cp.nimg, cp.K, cp.Kpad, cp.N, cp.relu, cp.in_ptrs, cp.in_off, cp.wgt, cp.bias, cp.out_ptrs, cp.out_off};
         st.gemv = true;
         e = launch_fc_gemv(fp, stream_);

@@ -529,58 +529,61 @@ cudaError_t launch_expand_rgb_many(const ExpandManyParams& p, cudaStream_t s) {
 }
 
 namespace {
+// One block per output column: its 256 threads split the weight row (K / 256
+// float4 each, all loads issued up front, so a whole 4-8 MB matrix is in
+// flight at once), per-image partial sums reduced across the block.
 __global__ void __launch_bounds__(256) fc_gemv_kernel(const FcParams p) {
   pdl::launch_dependents();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = blockIdx.x * 8 + warp;
-  const bool col = n < p.N;
-  const float* w = p.wgt + static_cast<long>(col ? n : 0) * p.Kpad;
-  // weights are immutable: the first slice is loaded before waiting for the
-  // previous kernel (the pooled inputs it writes)
-  float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (col && lane * 4 < p.K) w0 = __ldg(reinterpret_cast<const float4*>(w + lane * 4));
+  const int n = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const float* w = p.wgt + static_cast<long>(n) * p.Kpad;
+  constexpr int kMaxPer = 4;  // K <= 4096
+  float4 wv[kMaxPer];
+  // weights are immutable: loaded before waiting for the previous kernel
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int k = (u * 256 + t) * 4;
+    wv[u] = k < p.K ? __ldg(reinterpret_cast<const float4*>(w + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   pdl::wait();
-  if (!col) return;
-  float acc[kFcMaxImg];
-  const float* a[kFcMaxImg];
-#pragma unroll
-  for (int m = 0; m < kFcMaxImg; ++m) {
-    acc[m] = 0.f;
-    a[m] = m < p.nimg ? p.in_ptrs[m] + p.in_off : nullptr;
-  }
-  for (int k = lane * 4; k < p.K; k += 128) {
-    const float4 w4 = k == lane * 4 ? w0 : __ldg(reinterpret_cast<const float4*>(w + k));
-#pragma unroll
-    for (int m = 0; m < kFcMaxImg; ++m) {
-      if (m < p.nimg) {
-        const float4 x = *reinterpret_cast<const float4*>(a[m] + k);
-        acc[m] = fmaf(x.x, w4.x, acc[m]);
-        acc[m] = fmaf(x.y, w4.y, acc[m]);
-        acc[m] = fmaf(x.z, w4.z, acc[m]);
-        acc[m] = fmaf(x.w, w4.w, acc[m]);
-      }
-    }
-  }
-  const float b = p.bias ? __ldg(p.bias + n) : 0.f;
+  __shared__ float part[8][kFcMaxImg];
 #pragma unroll
   for (int m = 0; m < kFcMaxImg; ++m) {
     if (m >= p.nimg) break;
-    float v = acc[m];
+    const float* a = p.in_ptrs[m] + p.in_off;
+    float acc = 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) {
-      v += b;
-      if (p.relu == 1) v = fmaxf(v, 0.f);
-      else if (p.relu == 2) v = fminf(fmaxf(v, 0.f), 6.f);
-      p.out_ptrs[m][p.out_off + n] = v;
+    for (int u = 0; u < kMaxPer; ++u) {
+      const int k = (u * 256 + t) * 4;
+      if (k < p.K) {
+        const float4 x = *reinterpret_cast<const float4*>(a + k);
+        acc = fmaf(x.x, wv[u].x, acc);
+        acc = fmaf(x.y, wv[u].y, acc);
+        acc = fmaf(x.z, wv[u].z, acc);
+        acc = fmaf(x.w, wv[u].w, acc);
+      }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) part[warp][m] = acc;
+  }
+  __syncthreads();
+  if (t < p.nimg) {
+    float v = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += part[q][t];
+    if (p.bias) v += __ldg(p.bias + n);
+    if (p.relu == 1) v = fmaxf(v, 0.f);
+    else if (p.relu == 2) v = fminf(fmaxf(v, 0.f), 6.f);
+    p.out_ptrs[t][p.out_off + n] = v;
   }
 }
 }  // namespace
 
 cudaError_t launch_fc_gemv(const FcParams& p, cudaStream_t s) {
-  if (p.nimg <= 0 || p.nimg > kFcMaxImg || p.K % 4 || p.Kpad % 4 || p.in_off % 4) return cudaErrorInvalidValue;
-  return pdl::launch(fc_gemv_kernel, dim3((p.N + 7) / 8), dim3(256), 0, s, p);
+  if (p.nimg <= 0 || p.nimg > kFcMaxImg || p.K % 4 || p.Kpad % 4 || p.in_off % 4 || p.K > 4096)
+    return cudaErrorInvalidValue;
+  return pdl::launch(fc_gemv_kernel, dim3(p.N), dim3(256), 0, s, p);
 }
 
 cudaError_t launch_maxpool(const PoolParams& p, cudaStream_t s) {
