@@ -163,7 +163,7 @@ CONFIGS = {
         "workload": "config 2: GoogLeNet 224x224 single DNN, Poisson arrivals, Our-Tardy (on-time objective), "
                     "partial batching at layer granularity, B=90, 1 server per GPU"},
     3: {"suite": "resnet50_pair", "max_batch": 90, "deadline_ms": 7.072, "process": "pareto", "scheduler": "ours-time",
-        "granularity": "group", "shared_batching": True,
+        "granularity": "group", "shared_batching": True, "depth": 2,  # Pareto bursts: 2 in flight +4% (profiles/r02/serving_steps/depth_c3_sparse_sampling.txt)
         "workload": "config 3: two DNNs sharing a ResNet-50 backbone (heads 1000 / 365 classes), shared-layer "
                     "merge batching with riders, Pareto arrivals (alpha 1.25), G=5, B=90"},
     4: {"suite": "hetero3", "max_batch": 90, "deadline_ms": 6.949, "process": "poisson", "scheduler": "ours-time",
